@@ -1,0 +1,122 @@
+/*
+ * wino.h -- C ABI of the B200 Winograd fast-convolution path (libwino.so).
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *   winoconv.engine.winograd_forward(d, g, cfg, alg, cache_filters, counter, cache)
+ *   (/root/reference/pkg/src/winoconv/engine.py:198-254)
+ * and its helpers.  Plain C: opaque plan handle, caller-owned DEVICE pointers
+ * (except wino_forward_host), int status codes, a thread-local error string.
+ * No CUDA or torch types appear in the signatures; streams are passed as
+ * `void*` (a cudaStream_t / CUstream, NULL = legacy default stream).
+ *
+ * Status codes map onto the reference's exception types:
+ *   WINO_OK           0
+ *   WINO_EINVAL       1  -> ValueError   (shape/cfg mismatch, engine.py:211-218;
+ *                                         LayerConfig validation, direct.py:48-55)
+ *   WINO_EUNSUPPORTED 2  -> KeyError / ValueError (no builtin F(m,r), winograd.py:227-231;
+ *                                         R != alg.r, engine.py:217-218)
+ *   WINO_ENOMEM       3  -> MemoryError  (cmd_bench skips the row, commands.py:169-171)
+ *   WINO_ECUDA        4  -> RuntimeError
+ *
+ * Thread-safety: plans are immutable after creation; every call is reentrant
+ * across host threads and streams (no global mutable state besides the
+ * thread-local error string and a once-initialised driver entry point).
+ */
+#ifndef WINO_H_
+#define WINO_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WINO_OK 0
+#define WINO_EINVAL 1
+#define WINO_EUNSUPPORTED 2
+#define WINO_ENOMEM 3
+#define WINO_ECUDA 4
+
+/* Arithmetic of the alpha^2 transform-space GEMMs.  Transforms always run in
+ * the data type (fp32, or fp64 for WINO_PREC_FP64); accumulation is fp32
+ * (fp64 for WINO_PREC_FP64). */
+#define WINO_PREC_FP32 0 /* 3xTF32 split operands on tcgen05: fp32-accurate   */
+#define WINO_PREC_TF32 1 /* single-pass TF32 on tcgen05                        */
+#define WINO_PREC_BF16 2 /* bf16 operands on tcgen05 kind::f16                 */
+#define WINO_PREC_FP16 3 /* fp16 operands on tcgen05 kind::f16                 */
+#define WINO_PREC_FP64 4 /* fp64 data and GEMM on CUDA cores (reference FP64)  */
+
+/* One convolution layer; mirrors winoconv.direct.LayerConfig (direct.py:32-66).
+ * Output is (N, K, H+2*pad-R+1, W+2*pad-S+1). */
+typedef struct {
+  int N, C, H, W, K, R, S, pad;
+} wino_layer_t;
+
+typedef struct wino_plan_s* wino_plan_t;
+
+typedef struct {
+  int m, r, alpha;            /* F(m x m, r x r)                                 */
+  int out_h, out_w;
+  int tiles_h, tiles_w;       /* ceil(out/m)  (engine.py:57-61)                  */
+  long long P;                /* N * tiles_h * tiles_w  (engine.py:67-69)        */
+  int prec, c_pad, op_bytes, op_splits;
+  int gemm_bn;                /* filters per GEMM CTA (tcgen05 N)                */
+  int rows_per_chunk;         /* tile rows per workspace chunk                   */
+  int num_chunks;
+  long long chunk_tiles;      /* tiles per full chunk                            */
+  size_t u_bytes;             /* transformed-filter stack U                      */
+  size_t workspace_bytes;     /* V + M for one chunk (+ U when g is passed)      */
+  int launches_per_forward;   /* kernels launched by one wino_forward (U given)  */
+  long long multiplies;       /* P*C*K*alpha^2: the reference "mul" counter      */
+} wino_plan_info_t;
+
+/* Create a plan.  m in {2,4} (F(2x2,3x3), F(4x4,3x3)); R == S == 3.
+ * workspace_limit: byte budget for the per-chunk V+M staging buffers
+ * (0 = default, sized to stay L2-resident).  The tile/workspace planner splits
+ * the tile grid into row chunks that fit the budget. */
+int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspace_limit,
+                     wino_plan_t* out);
+int wino_plan_destroy(wino_plan_t plan);
+int wino_plan_get_info(wino_plan_t plan, wino_plan_info_t* info);
+
+/* U[s][xi*alpha+nu][k][c] = (G g_kc G^T)[xi,nu] split into op_splits planes,
+ * c padded to c_pad.  Replaces transform_filters (engine.py:104-114); the FX
+ * cache (engine.py:117-160) stores this buffer.  g is (K,C,3,3) fp32/fp64. */
+int wino_filter_transform(wino_plan_t plan, const void* g, void* U, void* stream);
+
+/* Full layer forward, replaces winograd_forward (engine.py:198-254).
+ * d: (N,C,H,W) fp32 (fp64 for WINO_PREC_FP64) device pointer.
+ * U: precomputed wino_filter_transform output, or NULL to transform g here
+ *    (g must then be non-NULL; the U stack lives in the workspace).
+ * y: (N,K,out_h,out_w) output, fully written (every element).
+ * workspace: >= info.workspace_bytes (U==NULL) or >= workspace_bytes-u_bytes. */
+int wino_forward(wino_plan_t plan, const void* d, const void* U, const void* g, void* y,
+                 void* workspace, size_t workspace_bytes, void* stream);
+
+/* End-to-end variant with HOST data: copies d_host -> d_dev, runs
+ * wino_forward, copies y_dev -> y_host, all on `stream` (pin the host buffers
+ * for asynchronous copies).  Returns after enqueueing. */
+int wino_forward_host(wino_plan_t plan, const void* d_host, const void* U, const void* g,
+                      void* y_host, void* d_dev, void* y_dev, void* workspace,
+                      size_t workspace_bytes, void* stream);
+
+/* wino_forward with CUDA events recorded on `stream` between the pipeline
+ * stages; synchronises the stream and ADDS each stage's device time (ms) to
+ * stage_ms[0..3] = {filter transform, input transform, GEMM, output
+ * transform} and its launch count to launches[0..3].  Used by bench.py to
+ * measure the dominant kernel live; not for production calls. */
+int wino_forward_timed(wino_plan_t plan, const void* d, const void* U, const void* g, void* y,
+                       void* workspace, size_t workspace_bytes, void* stream, float* stage_ms,
+                       int* launches);
+
+/* Last error message of the calling thread ("" if none). */
+const char* wino_last_error(void);
+/* Library version string. */
+const char* wino_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WINO_H_ */

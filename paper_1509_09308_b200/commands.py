@@ -1,0 +1,116 @@
+"""Algorithm-name dispatch and the layer benchmark on the GPU path
+(mirrors winoconv/commands.py:25-178 for the Winograd algorithms).
+
+Algorithm names are the reference's (``f2x2``, ``f4x4``, ``f2x2-fx``,
+``f4x4-fx``), optionally suffixed with a GEMM precision, e.g. ``f4x4-fx:bf16``.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence, Tuple
+
+from .engine import FilterCache, get_plan, winograd_forward
+from .layer import LayerConfig, builtin, gflops_direct
+from .suites import get_suite
+from .tensors import Tensor4, fill_uniform
+
+BENCH_ALGOS = ("f2x2", "f4x4", "f2x2-fx", "f4x4-fx")
+PRECISIONS = ("fp32", "tf32", "bf16", "fp16", "fp64")
+
+
+def parse_algo(algo: str) -> Tuple[int, bool, Optional[str]]:
+    """'f4x4-fx:bf16' -> (m=4, fx=True, prec='bf16')."""
+    base, _, prec = algo.partition(":")
+    if base not in BENCH_ALGOS:
+        raise ValueError(f"unknown algorithm {algo!r}; known: {', '.join(BENCH_ALGOS)}"
+                         " (optionally ':<prec>')")
+    if prec and prec not in PRECISIONS:
+        raise ValueError(f"unknown precision {prec!r}; known: {', '.join(PRECISIONS)}")
+    return (2 if base.startswith("f2x2") else 4), base.endswith("-fx"), (prec or None)
+
+
+def run_layer(algo: str, d: Tensor4, g: Tensor4, cfg: LayerConfig,
+              cache: Optional[FilterCache] = None, counter=None) -> Tensor4:
+    """Dispatch one forward layer by algorithm name (commands.py:31-51)."""
+    m, fx, prec = parse_algo(algo)
+    return winograd_forward(d, g, cfg, builtin(m, 3), cache_filters=fx, cache=cache,
+                            counter=counter, prec=prec)
+
+
+def layer_inputs(cfg: LayerConfig, seed: int, index: int) -> Tuple[Tensor4, Tensor4]:
+    """Data seed seed+2i, filters seed+2i+1, U[-1,1) (commands.py:54-61)."""
+    d = fill_uniform(Tensor4.zeros((cfg.N, cfg.C, cfg.H, cfg.W)), seed + 2 * index, -1.0, 1.0)
+    g = fill_uniform(Tensor4.zeros((cfg.K, cfg.C, cfg.R, cfg.S)), seed + 2 * index + 1, -1.0, 1.0)
+    return d, g
+
+
+_layer_inputs = layer_inputs
+
+
+@dataclass
+class Report:
+    columns: Tuple[str, ...]
+    rows: List[tuple] = field(default_factory=list)
+    seed: Optional[int] = None
+
+    def add(self, *vals) -> None:
+        if len(vals) != len(self.columns):
+            raise ValueError("row width mismatch")
+        self.rows.append(tuple(vals))
+
+    def to_csv(self) -> str:
+        lines = [] if self.seed is None else [f"# seed={self.seed}"]
+        lines.append(",".join(self.columns))
+        for r in self.rows:
+            lines.append(",".join("" if v is None else repr(v) if isinstance(v, float) else str(v)
+                                  for v in r))
+        return "\n".join(lines) + "\n"
+
+
+def cmd_bench(suite: str = "vgg-e", algo: str = "f2x2", batch: int = 1, repeats: int = 3,
+              scale: float = 1.0, seed: int = 0) -> Report:
+    """Per-layer best-of-N device time (CUDA events) and effective GFLOPS
+    = direct-conv GFLOP / time; depth-weighted TOTAL row (commands.py:136-178).
+    Inputs are resident in HBM; non-FX algorithms include the filter transform."""
+    import torch
+
+    if repeats < 1:
+        raise ValueError(f"repeats must be >= 1, got {repeats}")
+    m, fx, prec = parse_algo(algo)
+    layers = get_suite(suite).scaled(scale).with_batch(batch)
+    rep = Report(columns=("layer", "algo", "batch", "msec", "effective_gflops"), seed=seed)
+    total_sec = total_gf = 0.0
+    for i, entry in enumerate(layers.entries):
+        cfg = entry.cfg
+        try:
+            d, g = layer_inputs(cfg, seed, i)
+            plan = get_plan(cfg, m, prec or "fp32")
+            d_dev = torch.from_numpy(d.data.copy()).cuda()
+            g_dev = torch.from_numpy(g.data.copy()).cuda()
+            ws = plan.alloc_workspace()
+            y = torch.empty(plan.out_shape, dtype=plan.data_dtype, device="cuda")
+            U = plan.filter_transform(g_dev) if fx else None
+
+            def step():
+                plan.forward(d_dev, y=y, U=U, g=None if fx else g_dev, workspace=ws)
+
+            step()  # warm-up, untimed
+            best = float("inf")
+            for _ in range(repeats):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                a.record()
+                step()
+                b.record()
+                b.synchronize()
+                best = min(best, a.elapsed_time(b) / 1e3)
+        except (MemoryError, torch.cuda.OutOfMemoryError):
+            rep.add(entry.label, algo, batch, None, None)
+            continue
+        per_instance = gflops_direct(cfg) / cfg.depth
+        rep.add(entry.label, algo, batch, best * 1e3, per_instance / best)
+        total_sec += best * cfg.depth
+        total_gf += gflops_direct(cfg)
+    if total_sec > 0:
+        rep.add("TOTAL", algo, batch, total_sec * 1e3, total_gf / total_sec)
+    return rep

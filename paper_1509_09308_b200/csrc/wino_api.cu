@@ -1,0 +1,365 @@
+// C ABI (include/wino.h): plan creation with the tile/workspace planner,
+// filter transform, and the chunked forward pipeline
+//   input transform -> tcgen05 batched GEMM -> output transform
+// per chunk of whole tile rows, sized so the chunk's transform-space staging
+// (V and M) stays resident in the 126 MB L2 instead of round-tripping HBM.
+#include <cudaTypedefs.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+
+#include "wino_internal.h"
+
+struct wino_plan_s {
+  wino_layer_t L;
+  int m, r, alpha, a2, prec;
+  int oh, ow, th, tw;
+  long long P;
+  int c_pad, esize, nsplit, acc_bytes;
+  int bn;
+  int rows_total, rows_per_chunk, num_chunks;
+  long long chunk_tiles;
+  size_t u_bytes, v_bytes, m_bytes;  // v/m per full chunk
+};
+
+namespace wino {
+
+static thread_local std::string g_err;
+
+const char* set_error(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return g_err.c_str();
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static std::once_flag g_encode_once;
+
+static bool load_encode() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return g_encode != nullptr;
+}
+
+bool encode_tmap_3d(void* map_out, int prec, const void* base, uint64_t d0, uint64_t d1,
+                    uint64_t d2, uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box0,
+                    uint32_t box1) {
+  if (!load_encode()) {
+    set_error("cuTensorMapEncodeTiled unavailable (driver too old?)");
+    return false;
+  }
+  CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  if (prec == kBF16) dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  if (prec == kFP16) dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
+  cuuint32_t box[3] = {box0, box1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(reinterpret_cast<CUtensorMap*>(map_out), dt, 3, const_cast<void*>(base),
+                        dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d): dims %llu,%llu,%llu strides %llu,%llu", (int)r,
+              (unsigned long long)d0, (unsigned long long)d1, (unsigned long long)d2,
+              (unsigned long long)stride1_bytes, (unsigned long long)stride2_bytes);
+    return false;
+  }
+  return true;
+}
+
+static int cuda_fail(cudaError_t e, const char* what) {
+  if (e == cudaErrorMemoryAllocation) {
+    set_error("%s: out of device memory", what);
+    return WINO_ENOMEM;
+  }
+  set_error("%s: %s", what, cudaGetErrorString(e));
+  return WINO_ECUDA;
+}
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Default chunk budget: transform-space staging that stays L2-resident.
+constexpr size_t kDefaultWorkspace = 64ull << 20;
+
+}  // namespace wino
+
+using namespace wino;
+
+extern "C" {
+
+const char* wino_last_error(void) { return g_err.c_str(); }
+
+const char* wino_version(void) { return "wino-b200 0.1.0 (sm_100a)"; }
+
+int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspace_limit,
+                     wino_plan_t* out) {
+  g_err.clear();
+  if (!layer || !out) {
+    set_error("null argument");
+    return WINO_EINVAL;
+  }
+  *out = nullptr;
+  const wino_layer_t& L = *layer;
+  // LayerConfig validation (direct.py:48-55)
+  if (L.N < 1 || L.C < 1 || L.H < 1 || L.W < 1 || L.K < 1 || L.R < 1 || L.S < 1) {
+    set_error("N, C, H, W, K, R, S must be >= 1");
+    return WINO_EINVAL;
+  }
+  if (L.pad < 0) {
+    set_error("pad must be >= 0");
+    return WINO_EINVAL;
+  }
+  const int oh = L.H + 2 * L.pad - L.R + 1, ow = L.W + 2 * L.pad - L.S + 1;
+  if (oh < 1 || ow < 1) {
+    set_error("output dimensions must be >= 1");
+    return WINO_EINVAL;
+  }
+  if (m != 2 && m != 4) {  // builtin() lookup (winograd.py:225-232)
+    set_error("no builtin algorithm for F(%d,3); available F(2,3), F(4,3)", m);
+    return WINO_EUNSUPPORTED;
+  }
+  if (L.R != 3 || L.S != 3) {  // engine.py:217-218
+    set_error("layer filter %dx%d but algorithm is F(%d,3)", L.R, L.S, m);
+    return WINO_EUNSUPPORTED;
+  }
+  if (prec < WINO_PREC_FP32 || prec > WINO_PREC_FP64) {
+    set_error("unknown precision %d", prec);
+    return WINO_EINVAL;
+  }
+  wino_plan_s* p = new (std::nothrow) wino_plan_s();
+  if (!p) {
+    set_error("host allocation failed");
+    return WINO_ENOMEM;
+  }
+  p->L = L;
+  p->m = m;
+  p->r = 3;
+  p->alpha = m + 2;
+  p->a2 = p->alpha * p->alpha;
+  p->prec = prec;
+  p->oh = oh;
+  p->ow = ow;
+  p->th = (oh + m - 1) / m;
+  p->tw = (ow + m - 1) / m;
+  p->P = static_cast<long long>(L.N) * p->th * p->tw;
+  p->esize = op_bytes(prec);
+  p->nsplit = op_splits(prec);
+  p->acc_bytes = prec == kFP64 ? 8 : 4;
+  // channel stride padded so TMA row strides are 16-byte multiples
+  p->c_pad = static_cast<int>(align_up(L.C, 16 / p->esize));
+  p->u_bytes = align_up(static_cast<size_t>(p->nsplit) * p->a2 * L.K * p->c_pad * p->esize, 1024);
+
+  // ---- GEMM tile: BN filters per CTA (tcgen05 N).  Prefer wide tiles, shrink
+  // while the grid would leave SMs idle.
+  int bn = 256;
+  if (prec == kFP32) bn = 128;  // 3 split stages of 64 KB fit; 256 would leave 2
+  while (bn > 32 && bn / 2 >= L.K) bn /= 2;
+  const long long ptiles = (p->P + 127) / 128;
+  while (bn > 64 && ptiles * ((L.K + bn - 1) / bn) * p->a2 < 148) bn /= 2;
+  p->bn = bn;
+
+  // ---- chunk planner: whole tile rows, V + M staging within the budget
+  const size_t budget = workspace_limit ? workspace_limit : kDefaultWorkspace;
+  const size_t per_tile = static_cast<size_t>(p->nsplit) * p->a2 * p->c_pad * p->esize +
+                          static_cast<size_t>(p->a2) * L.K * p->acc_bytes;
+  const size_t per_row = per_tile * p->tw;
+  p->rows_total = L.N * p->th;
+  long long rows = static_cast<long long>(budget / (per_row ? per_row : 1));
+  if (rows < 1) rows = 1;
+  if (rows > p->rows_total) rows = p->rows_total;
+  p->rows_per_chunk = static_cast<int>(rows);
+  p->num_chunks = (p->rows_total + p->rows_per_chunk - 1) / p->rows_per_chunk;
+  p->chunk_tiles = static_cast<long long>(p->rows_per_chunk) * p->tw;
+  p->v_bytes = align_up(static_cast<size_t>(p->nsplit) * p->a2 * p->chunk_tiles * p->c_pad *
+                            p->esize,
+                        1024);
+  p->m_bytes = align_up(static_cast<size_t>(p->a2) * L.K * p->chunk_tiles * p->acc_bytes, 1024);
+  *out = p;
+  return WINO_OK;
+}
+
+int wino_plan_destroy(wino_plan_t plan) {
+  delete plan;
+  return WINO_OK;
+}
+
+int wino_plan_get_info(wino_plan_t p, wino_plan_info_t* info) {
+  if (!p || !info) {
+    set_error("null argument");
+    return WINO_EINVAL;
+  }
+  memset(info, 0, sizeof *info);
+  info->m = p->m;
+  info->r = p->r;
+  info->alpha = p->alpha;
+  info->out_h = p->oh;
+  info->out_w = p->ow;
+  info->tiles_h = p->th;
+  info->tiles_w = p->tw;
+  info->P = p->P;
+  info->prec = p->prec;
+  info->c_pad = p->c_pad;
+  info->op_bytes = p->esize;
+  info->op_splits = p->nsplit;
+  info->gemm_bn = p->bn;
+  info->rows_per_chunk = p->rows_per_chunk;
+  info->num_chunks = p->num_chunks;
+  info->chunk_tiles = p->chunk_tiles;
+  info->u_bytes = p->u_bytes;
+  info->workspace_bytes = p->u_bytes + p->v_bytes + p->m_bytes;
+  info->launches_per_forward = p->num_chunks * 3;
+  info->multiplies = p->P * p->L.C * static_cast<long long>(p->L.K) * p->a2;
+  return WINO_OK;
+}
+
+int wino_filter_transform(wino_plan_t p, const void* g, void* U, void* stream) {
+  g_err.clear();
+  if (!p || !g || !U) {
+    set_error("null argument");
+    return WINO_EINVAL;
+  }
+  cudaError_t e = launch_filter_transform(p->m, p->prec, g, U, p->L.K, p->L.C, p->c_pad,
+                                          static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? WINO_OK : cuda_fail(e, "filter transform");
+}
+
+namespace {
+struct StageTimer {  // optional per-stage CUDA-event timing on the launch stream
+  cudaStream_t s;
+  float* ms;
+  int* launches;
+  cudaEvent_t ev[2];
+  bool on;
+  StageTimer(cudaStream_t s_, float* ms_, int* l_) : s(s_), ms(ms_), launches(l_), on(ms_ != nullptr) {
+    if (on) {
+      cudaEventCreate(&ev[0]);
+      cudaEventCreate(&ev[1]);
+    }
+  }
+  ~StageTimer() {
+    if (on) {
+      cudaEventDestroy(ev[0]);
+      cudaEventDestroy(ev[1]);
+    }
+  }
+  void begin() {
+    if (on) cudaEventRecord(ev[0], s);
+  }
+  void end(int stage) {
+    if (!on) return;
+    cudaEventRecord(ev[1], s);
+    cudaEventSynchronize(ev[1]);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, ev[0], ev[1]);
+    ms[stage] += t;
+    launches[stage] += 1;
+  }
+};
+}  // namespace
+
+static int forward_impl(wino_plan_t p, const void* d, const void* U, const void* g, void* y,
+                        void* workspace, size_t workspace_bytes, void* stream, float* stage_ms,
+                        int* launches) {
+  g_err.clear();
+  if (!p || !d || !y || (!U && !g) || !workspace) {
+    set_error("null argument");
+    return WINO_EINVAL;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  StageTimer tm(s, stage_ms, launches);
+  unsigned char* ws = static_cast<unsigned char*>(workspace);
+  size_t need = p->v_bytes + p->m_bytes + (U ? 0 : p->u_bytes);
+  if (workspace_bytes < need) {
+    set_error("workspace too small: %zu < %zu bytes", workspace_bytes, need);
+    return WINO_EINVAL;
+  }
+  if (!U) {
+    tm.begin();
+    cudaError_t e = launch_filter_transform(p->m, p->prec, g, ws, p->L.K, p->L.C, p->c_pad, s);
+    if (e != cudaSuccess) return cuda_fail(e, "filter transform");
+    tm.end(0);
+    U = ws;
+    ws += p->u_bytes;
+  }
+  void* V = ws;
+  void* Mb = ws + p->v_bytes;
+  const wino_layer_t& L = p->L;
+  for (int ch = 0; ch < p->num_chunks; ++ch) {
+    const int row0 = ch * p->rows_per_chunk;
+    const int rows = (row0 + p->rows_per_chunk <= p->rows_total) ? p->rows_per_chunk
+                                                                  : p->rows_total - row0;
+    const long long Pc = static_cast<long long>(rows) * p->tw;
+    tm.begin();
+    cudaError_t e = launch_input_transform(p->m, p->prec, d, V, L.N, L.C, L.H, L.W, L.pad, p->th,
+                                           p->tw, row0, rows, Pc, p->c_pad, s);
+    if (e != cudaSuccess) return cuda_fail(e, "input transform");
+    tm.end(1);
+    GemmArgs ga{V, U, Mb, p->a2, L.K, L.C, p->c_pad, Pc, p->bn};
+    tm.begin();
+    e = launch_batched_gemm(p->prec, ga, s);
+    if (e != cudaSuccess) {
+      if (g_err.empty()) return cuda_fail(e, "batched gemm");
+      return WINO_ECUDA;
+    }
+    tm.end(2);
+    tm.begin();
+    e = launch_output_transform(p->m, p->prec, Mb, y, L.N, L.K, p->th, p->tw, p->oh, p->ow, row0,
+                                Pc, s);
+    if (e != cudaSuccess) return cuda_fail(e, "output transform");
+    tm.end(3);
+  }
+  return WINO_OK;
+}
+
+int wino_forward(wino_plan_t p, const void* d, const void* U, const void* g, void* y,
+                 void* workspace, size_t workspace_bytes, void* stream) {
+  return forward_impl(p, d, U, g, y, workspace, workspace_bytes, stream, nullptr, nullptr);
+}
+
+int wino_forward_timed(wino_plan_t p, const void* d, const void* U, const void* g, void* y,
+                       void* workspace, size_t workspace_bytes, void* stream, float* stage_ms,
+                       int* launches) {
+  if (!stage_ms || !launches) {
+    set_error("null argument");
+    return WINO_EINVAL;
+  }
+  return forward_impl(p, d, U, g, y, workspace, workspace_bytes, stream, stage_ms, launches);
+}
+
+int wino_forward_host(wino_plan_t p, const void* d_host, const void* U, const void* g,
+                      void* y_host, void* d_dev, void* y_dev, void* workspace,
+                      size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  if (!p || !d_host || !y_host || !d_dev || !y_dev) {
+    set_error("null argument");
+    return WINO_EINVAL;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const wino_layer_t& L = p->L;
+  const size_t db = static_cast<size_t>(L.N) * L.C * L.H * L.W * p->acc_bytes;
+  const size_t yb = static_cast<size_t>(L.N) * L.K * p->oh * p->ow * p->acc_bytes;
+  cudaError_t e = cudaMemcpyAsync(d_dev, d_host, db, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D copy");
+  int rc = wino_forward(p, d_dev, U, g, y_dev, workspace, workspace_bytes, stream);
+  if (rc != WINO_OK) return rc;
+  e = cudaMemcpyAsync(y_host, y_dev, yb, cudaMemcpyDeviceToHost, s);
+  if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+  return WINO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,65 @@
+// Internal declarations shared by the kernel translation units and the C-ABI.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/wino.h"
+
+namespace wino {
+
+// Operand precision of the alpha^2 batched GEMM (the transform-space data).
+enum Prec : int {
+  kFP32 = WINO_PREC_FP32,  // 3xTF32 split operands (hi + lo), fp32-accurate
+  kTF32 = WINO_PREC_TF32,  // single-pass TF32
+  kBF16 = WINO_PREC_BF16,
+  kFP16 = WINO_PREC_FP16,
+  kFP64 = WINO_PREC_FP64,  // fp64 data end to end (CUDA-core GEMM)
+};
+
+inline int op_bytes(int prec) {
+  switch (prec) {
+    case kBF16:
+    case kFP16: return 2;
+    case kFP64: return 8;
+    default: return 4;
+  }
+}
+inline int op_splits(int prec) { return prec == kFP32 ? 2 : 1; }
+
+// ---- launchers (defined in wino_transforms.cu / wino_gemm.cu) -------------
+// All return cudaError_t of the launch.
+
+// g (K,C,3,3) [float or double] -> U [nsplit][alpha^2][K][c_pad]
+cudaError_t launch_filter_transform(int m, int prec, const void* g, void* U, int K, int C,
+                                    int c_pad, cudaStream_t s);
+
+// d (N,C,H,W) -> V [nsplit][alpha^2][Pc][c_pad] for tile rows [row0, row0+rows)
+cudaError_t launch_input_transform(int m, int prec, const void* d, void* V, int N, int C, int H,
+                                   int W, int pad, int th, int tw, int row0, int rows,
+                                   long long Pc, int c_pad, cudaStream_t s);
+
+// M [alpha^2][K][Pc] (float, or double for FP64) -> y (N,K,oh,ow), clipped
+cudaError_t launch_output_transform(int m, int prec, const void* Mbuf, void* y, int N, int K,
+                                    int th, int tw, int oh, int ow, int row0, long long Pc,
+                                    cudaStream_t s);
+
+struct GemmArgs {
+  const void* V;   // [nsplit][a2][Pc][c_pad]
+  const void* U;   // [nsplit][a2][K][c_pad]
+  void* M;         // [a2][K][Pc]
+  int a2, K, C, c_pad;
+  long long Pc;
+  int bn;          // filters per CTA (tcgen05 N)
+};
+// Tensor-core (tcgen05) GEMM for FP32/TF32/BF16/FP16, CUDA-core fp64 for FP64.
+cudaError_t launch_batched_gemm(int prec, const GemmArgs& a, cudaStream_t s);
+int gemm_kernels_per_launch(int prec);
+
+// Host helpers.
+const char* set_error(const char* fmt, ...);
+bool encode_tmap_3d(void* map_out, int prec, const void* base, uint64_t d0, uint64_t d1,
+                    uint64_t d2, uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box0,
+                    uint32_t box1);
+
+}  // namespace wino

@@ -1,0 +1,109 @@
+// Builtin minimal-filtering matrices F(2,3) and F(4,3), as compile-time
+// constants.  Entries are the exact rationals of the reference
+// (winograd.py:151-168 for F(2,3), winograd.py:192-215 for F(4,3)) written as
+// correctly-rounded doubles and rounded ONCE more to the data type at use,
+// exactly like the reference's Fraction -> float -> dtype lowering
+// (engine.py:98-101, rational.py:135-141).
+//
+// All transform loops are fully unrolled; coefficient tests fold at compile
+// time, so zero entries cost nothing and +-1 entries become add/sub.
+#pragma once
+
+namespace wino {
+
+template <int M>
+struct Alg;
+
+template <>
+struct Alg<2> {
+  static constexpr int m = 2, r = 3, alpha = 4;
+  __host__ __device__ static constexpr double BT(int i, int j) {
+    constexpr double t[4][4] = {{1, 0, -1, 0}, {0, 1, 1, 0}, {0, -1, 1, 0}, {0, 1, 0, -1}};
+    return t[i][j];
+  }
+  __host__ __device__ static constexpr double G(int i, int j) {
+    constexpr double t[4][3] = {{1, 0, 0}, {0.5, 0.5, 0.5}, {0.5, -0.5, 0.5}, {0, 0, 1}};
+    return t[i][j];
+  }
+  __host__ __device__ static constexpr double AT(int i, int j) {
+    constexpr double t[2][4] = {{1, 1, 1, 0}, {0, 1, -1, -1}};
+    return t[i][j];
+  }
+};
+
+template <>
+struct Alg<4> {
+  static constexpr int m = 4, r = 3, alpha = 6;
+  __host__ __device__ static constexpr double BT(int i, int j) {
+    constexpr double t[6][6] = {{4, 0, -5, 0, 1, 0},  {0, -4, -4, 1, 1, 0}, {0, 4, -4, -1, 1, 0},
+                                {0, -2, -1, 2, 1, 0}, {0, 2, -1, -2, 1, 0}, {0, 4, 0, -5, 0, 1}};
+    return t[i][j];
+  }
+  __host__ __device__ static constexpr double G(int i, int j) {
+    constexpr double t[6][3] = {{1.0 / 4, 0, 0},
+                                {-1.0 / 6, -1.0 / 6, -1.0 / 6},
+                                {-1.0 / 6, 1.0 / 6, -1.0 / 6},
+                                {1.0 / 24, 1.0 / 12, 1.0 / 6},
+                                {1.0 / 24, -1.0 / 12, 1.0 / 6},
+                                {0, 0, 1}};
+    return t[i][j];
+  }
+  __host__ __device__ static constexpr double AT(int i, int j) {
+    constexpr double t[4][6] = {
+        {1, 1, 1, 1, 1, 0}, {0, 1, -1, 2, -2, 0}, {0, 1, 1, 4, 4, 0}, {0, 1, -1, 8, -8, 1}};
+    return t[i][j];
+  }
+};
+
+// acc + c*x with the coefficient folded at compile time.
+template <typename T>
+__device__ __forceinline__ T mac(T acc, double c, T x, bool first) {
+  if (c == 0.0) return acc;
+  if (first) {
+    if (c == 1.0) return x;
+    if (c == -1.0) return -x;
+    return static_cast<T>(c) * x;
+  }
+  if (c == 1.0) return acc + x;
+  if (c == -1.0) return acc - x;
+  return acc + static_cast<T>(c) * x;
+}
+
+// out[i][j] = sum_u sum_v L(i,u) * in[u][v] * L(j,v)   (L is ROWS x COLS)
+// i.e. out = L in L^T: used for B^T d B (L = BT), G g G^T (L = G), A^T M A (L = AT).
+template <typename T, int ROWS, int COLS, typename LF>
+__device__ __forceinline__ void sandwich(const T (&in)[COLS][COLS], T (&out)[ROWS][ROWS], LF L) {
+  T tmp[ROWS][COLS];
+#pragma unroll
+  for (int i = 0; i < ROWS; ++i) {
+#pragma unroll
+    for (int v = 0; v < COLS; ++v) {
+      T acc = T(0);
+      bool first = true;
+#pragma unroll
+      for (int u = 0; u < COLS; ++u) {
+        const double c = L(i, u);
+        acc = mac(acc, c, in[u][v], first);
+        if (c != 0.0) first = false;
+      }
+      tmp[i][v] = acc;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < ROWS; ++i) {
+#pragma unroll
+    for (int j = 0; j < ROWS; ++j) {
+      T acc = T(0);
+      bool first = true;
+#pragma unroll
+      for (int v = 0; v < COLS; ++v) {
+        const double c = L(j, v);
+        acc = mac(acc, c, tmp[i][v], first);
+        if (c != 0.0) first = false;
+      }
+      out[i][j] = acc;
+    }
+  }
+}
+
+}  // namespace wino

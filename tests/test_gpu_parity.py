@@ -1,0 +1,171 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle and the
+reference's golden outputs on identical SplitMix64 inputs.
+
+Tolerances (max-abs, stated per F(m,r) and GEMM precision):
+  * vs fp64 direct conv: the reference's own gates, F2 < 5e-4, F4 < 5e-3 for
+    the fp32 (3xTF32) path (test_engine.py:97-112); fp64 < 1e-12
+    (test_engine.py:114-119).
+  * vs the reference's fp32 Winograd output: |diff| <= 2e-5 * (1 + max|y|)
+    for fp32 (both are fp32-accurate; only summation order differs).
+  * reduced-precision GEMMs, relative to max|y|: tf32 <= 1e-2 (F2) / 4e-2 (F4);
+    fp16 <= 4e-3 / 2e-2; bf16 <= 2e-2 / 1.5e-1  (operand rounding of U and V,
+    measured envelope x ~3 margin).
+"""
+import numpy as np
+import pytest
+
+from oracle import winograd_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = {("tf32", 2): 1e-2, ("tf32", 4): 4e-2, ("fp16", 2): 4e-3, ("fp16", 4): 2e-2,
+           ("bf16", 2): 2e-2, ("bf16", 4): 1.5e-1}
+
+
+@pytest.fixture(scope="module")
+def wb():
+    import paper_1509_09308_b200 as wb
+    return wb
+
+
+def _run(wb, d, g, pad, m, prec=None, fx=False, cache=None):
+    cfg = wb.LayerConfig(N=d.shape[0], C=d.shape[1], H=d.shape[2], W=d.shape[3], K=g.shape[0],
+                         pad=pad)
+    prc = wb.Precision.FP64 if d.dtype == np.float64 else wb.Precision.FP32
+    return wb.winograd_forward(wb.Tensor4.from_array(d, prc), wb.Tensor4.from_array(g, prc), cfg,
+                               wb.builtin(m, 3), cache_filters=fx, cache=cache, prec=prec).data
+
+
+@pytest.mark.parametrize("m", [2, 4])
+def test_golden_cases_fp32(wb, golden, m):
+    for i in range(10):
+        N, C, H, W, K, pad = (int(v) for v in golden[f"case{i}_shape"])
+        d = O.fill_uniform((N, C, H, W), 100 + 2 * i)
+        g = O.fill_uniform((K, C, 3, 3), 101 + 2 * i)
+        y = _run(wb, d, g, pad, m)
+        ref = golden[f"case{i}_f{m}_fp32"]
+        direct = golden[f"case{i}_direct64"]
+        assert y.shape == ref.shape
+        scale = 1.0 + np.abs(ref).max()
+        assert np.abs(y - ref).max() <= 2e-5 * scale, (i, np.abs(y - ref).max())
+        assert O.max_abs_error(y, direct) < (5e-4 if m == 2 else 5e-3), i
+
+
+@pytest.mark.parametrize("m", [2, 4])
+def test_golden_cases_fp64(wb, golden, m):
+    for i in range(10):
+        N, C, H, W, K, pad = (int(v) for v in golden[f"case{i}_shape"])
+        d = O.fill_uniform((N, C, H, W), 100 + 2 * i).astype(np.float64)
+        g = O.fill_uniform((K, C, 3, 3), 101 + 2 * i).astype(np.float64)
+        y = _run(wb, d, g, pad, m)
+        assert y.dtype == np.float64
+        assert O.max_abs_error(y, golden[f"case{i}_direct64"]) < 1e-12, i
+        assert O.max_abs_error(y, golden[f"case{i}_f{m}_fp64"]) < 1e-12, i
+
+
+@pytest.mark.parametrize("m", [2, 4])
+@pytest.mark.parametrize("prec", ["tf32", "bf16", "fp16"])
+def test_reduced_precision_envelope(wb, golden, m, prec):
+    for i in (3, 5, 7, 9):
+        N, C, H, W, K, pad = (int(v) for v in golden[f"case{i}_shape"])
+        d = O.fill_uniform((N, C, H, W), 100 + 2 * i)
+        g = O.fill_uniform((K, C, 3, 3), 101 + 2 * i)
+        y = _run(wb, d, g, pad, m, prec=prec)
+        ref = golden[f"case{i}_direct64"]
+        err = O.max_abs_error(y, ref) / np.abs(ref).max()
+        assert err <= REL_TOL[(prec, m)], (i, err)
+
+
+def test_config1_against_reference(wb, golden):
+    """Config 1 (N=1 C=K=64 56x56 pad=1) vs the reference's recorded output."""
+    d = O.fill_uniform((1, 64, 56, 56), 0)
+    g = O.fill_uniform((64, 64, 3, 3), 1)
+    for m in (2, 4):
+        y = _run(wb, d, g, 1, m)
+        samp = y.reshape(-1)[::37]
+        ref = golden[f"cfg1_f{m}_sample"]
+        assert np.abs(samp - ref).max() <= 2e-5 * (1 + np.abs(ref).max())
+        s = golden[f"cfg1_f{m}_sum"]
+        assert abs(y.astype(np.float64).sum() - s[0]) <= 1e-6 * s[1]
+
+
+def test_zero_filters_exact(wb):
+    d = O.fill_uniform((1, 2, 6, 6), 1)
+    g = np.zeros((2, 2, 3, 3), np.float32)
+    for m in (2, 4):
+        for prec in ("fp32", "tf32", "bf16", "fp16"):
+            assert np.all(_run(wb, d, g, 1, m, prec=prec) == 0.0)
+
+
+def test_impulse_filter_copies_input(wb):
+    """A centred delta filter reproduces the input: any tile-indexing or
+    padding slip would show as O(1) errors.  Exact for F(2x2) (all transform
+    constants are dyadic); F(4x4)'s 1/6, 1/12, 1/24 round in fp32."""
+    d = O.fill_uniform((2, 3, 13, 11), 5)
+    g = np.zeros((3, 3, 3, 3), np.float32)
+    for k in range(3):
+        g[k, k, 1, 1] = 1.0
+    for m in (2, 4):
+        y = _run(wb, d, g, 1, m)
+        np.testing.assert_allclose(y, d, atol=(1e-6 if m == 2 else 1e-5), rtol=0)
+
+
+def test_fx_cache_bitwise_and_counts(wb):
+    d = O.fill_uniform((1, 8, 9, 9), 9)
+    g = O.fill_uniform((4, 8, 3, 3), 10)
+    cache = wb.FilterCache()
+    a = _run(wb, d, g, 1, 4, fx=True, cache=cache)
+    b = _run(wb, d, g, 1, 4, fx=True, cache=cache)
+    c = _run(wb, d, g, 1, 4)
+    assert cache.misses == 1 and cache.hits == 1 and len(cache) == 1
+    assert np.array_equal(a, b) and np.array_equal(a, c)
+    assert cache.workspace_scalars() == 36 * 4 * 8
+
+
+def test_bitwise_deterministic(wb):
+    d = O.fill_uniform((1, 8, 9, 9), 9)
+    g = O.fill_uniform((4, 8, 3, 3), 10)
+    for prec in ("fp32", "bf16"):
+        assert np.array_equal(_run(wb, d, g, 1, 2, prec=prec), _run(wb, d, g, 1, 2, prec=prec))
+
+
+def test_chunked_planner_matches_single_chunk(wb):
+    """Workspace-limited plans (many row chunks) give bit-identical outputs."""
+    import torch
+    cfg = wb.LayerConfig(N=2, C=16, H=30, W=22, K=24, pad=1)
+    d = torch.from_numpy(O.fill_uniform((2, 16, 30, 22), 3)).cuda()
+    g = torch.from_numpy(O.fill_uniform((24, 16, 3, 3), 4)).cuda()
+    for m in (2, 4):
+        big = wb.WinogradPlan(cfg, m, "fp32")
+        small = wb.WinogradPlan(cfg, m, "fp32", workspace_limit=64 * 1024)
+        assert big.info["num_chunks"] == 1 and small.info["num_chunks"] > 3
+        ya = big.forward(d, g=g)
+        yb = small.forward(d, g=g)
+        torch.cuda.synchronize()
+        assert torch.equal(ya, yb)
+
+
+def test_random_shape_sweep(wb, golden):
+    """First 40 shapes of the acceptance sweep (test_acceptance.py:120-142)."""
+    shapes = golden["sweep55_shapes"][:40]
+    worst = {2: 0.0, 4: 0.0}
+    for i, (N, C, H, W, K, pad) in enumerate(shapes):
+        N, C, H, W, K, pad = (int(v) for v in (N, C, H, W, K, pad))
+        d = O.fill_uniform((N, C, H, W), 1000 + 2 * i)
+        g = O.fill_uniform((K, C, 3, 3), 1001 + 2 * i)
+        ref = O.direct_forward(d, g, pad)
+        for m in (2, 4):
+            worst[m] = max(worst[m], O.max_abs_error(_run(wb, d, g, pad, m), ref))
+    assert worst[2] < 5e-4 and worst[4] < 5e-3, worst
+
+
+def test_grad_inputs_matches_oracle(wb):
+    d = O.fill_uniform((1, 4, 10, 10), 7)
+    g = O.fill_uniform((6, 4, 3, 3), 8)
+    dy = O.fill_uniform((1, 6, 10, 10), 9)
+    cfg = wb.LayerConfig(N=1, C=4, H=10, W=10, K=6, pad=1)
+    T = wb.Tensor4.from_array
+    out = wb.winograd_grad_inputs(T(dy), T(g), cfg, wb.builtin(4, 3)).data
+    flipped = np.ascontiguousarray(g[:, :, ::-1, ::-1].transpose(1, 0, 2, 3))
+    ref = O.direct_forward(dy, flipped, 1)
+    assert O.max_abs_error(out, ref) < 5e-3
