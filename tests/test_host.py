@@ -1,0 +1,194 @@
+"""Host-side logic of the drop-in (no GPU needed): interface types, tile
+grid, planner, validation errors -- mirroring the reference's unit tests
+(test_engine.py:17-71,128-139; test_tensors.py; test_suites.py)."""
+import re
+
+import numpy as np
+import pytest
+
+import paper_1509_09308_b200 as wb
+from paper_1509_09308_b200 import engine, sharding
+
+
+def rand(shape, seed, prec=wb.Precision.FP32):
+    return wb.fill_uniform(wb.Tensor4.zeros(shape, precision=prec), seed, -1.0, 1.0)
+
+
+def test_fill_uniform_matches_reference(golden):
+    assert np.array_equal(rand((2, 3, 5, 7), 3).data, golden["fill_f32_s3"])
+    assert np.array_equal(rand((1, 2, 3, 4), 4, wb.Precision.FP64).data, golden["fill_f64_s4"])
+    t = wb.fill_uniform(wb.Tensor4.zeros((1, 1, 4, 64)), 9, -0.5, 2.0)
+    assert np.array_equal(t.data, golden["fill_f32_lohi"])
+    assert np.array_equal(wb.quantize_fp16(rand((1, 2, 8, 8), 11)).data, golden["fp16_q"])
+
+
+def test_tensor4_contract():
+    t = rand((1, 2, 3, 4), 1)
+    assert not t.data.flags.writeable
+    with pytest.raises(IndexError):
+        t[0, 2, 0, 0]
+    with pytest.raises(ValueError):
+        wb.Tensor4(np.zeros((2, 2)), wb.Precision.FP32)
+    with pytest.raises(ValueError):
+        wb.fill_uniform(t, 0, 1.0, 1.0)
+    with pytest.raises(OverflowError):
+        wb.quantize_fp16(wb.Tensor4.from_array(np.full((1, 1, 1, 1), 1e6)))
+
+
+@pytest.mark.parametrize("mr", [(2, 3), (4, 3)])
+def test_builtin_matrices_match_reference(golden, mr):
+    m, r = mr
+    alg = wb.builtin(m, r)
+    for dt in (np.float32, np.float64):
+        BT, G, AT = alg.lowered(dt)
+        tag = np.dtype(dt).name
+        assert np.array_equal(BT, golden[f"BT_{m}{r}_{tag}"])
+        assert np.array_equal(G, golden[f"G_{m}{r}_{tag}"])
+        assert np.array_equal(AT, golden[f"AT_{m}{r}_{tag}"])
+    assert alg.alpha == m + 2
+
+
+def test_cuda_constants_match_reference(golden):
+    """The kernels' compiled-in matrices (csrc/winograd_mats.cuh) equal the
+    reference's lowered matrices entry by entry."""
+    import os
+    src = open(os.path.join(os.path.dirname(wb.__file__), "csrc", "winograd_mats.cuh")).read()
+    for m, r, n in ((2, 3, 4), (4, 3, 6)):
+        body = src[src.index(f"struct Alg<{m}>"):]
+        for name, rows in (("BT", n), ("G", n), ("AT", m)):
+            blk = body[body.index(f"double {name}("):]
+            blk = blk[blk.index("= {") + 2: blk.index("};")]
+            vals = [eval(v) for v in re.findall(r"-?[\d.]+(?:\s*/\s*\d+)?", blk)]
+            ref = golden[f"{name}_{m}{r}_float64"]
+            assert np.array_equal(np.array(vals).reshape(ref.shape), ref), (m, name)
+            assert np.array_equal(np.array(vals, np.float32).reshape(ref.shape),
+                                  golden[f"{name}_{m}{r}_float32"])
+
+
+def test_unknown_builtin():
+    with pytest.raises(KeyError):
+        wb.builtin(3, 3)
+
+
+def test_tile_grid_matches_reference(golden):
+    for row in golden["tile_grid"]:
+        N, C, H, W, K, pad, m, th, tw, P, tc, mul, b, n, ty, tx, oy, ox = (int(v) for v in row)
+        cfg = wb.LayerConfig(N=N, C=C, H=H, W=W, K=K, pad=pad)
+        grid = wb.TileGrid.for_layer(cfg, m, 3)
+        assert (grid.tiles_h, grid.tiles_w, grid.P) == (th, tw, P)
+        assert wb.tile_count(cfg, m) == tc
+        assert wb.multiply_stage_flops(cfg, m) == mul
+        assert grid.index(b) == (n, ty, tx) and grid.origin(b) == (oy, ox)
+    with pytest.raises(IndexError):
+        grid.index(grid.P)
+
+
+def test_reference_counts():
+    # test_engine.py:47-58
+    assert wb.tile_count(wb.LayerConfig(N=1, C=1, H=224, W=224, K=1, pad=1), 2) == 12544
+    assert wb.tile_count(wb.LayerConfig(N=1, C=1, H=14, W=14, K=1, pad=1), 4) == 16
+    cfg = wb.LayerConfig(N=2, C=3, H=9, W=7, K=5, pad=1)
+    assert wb.multiply_stage_flops(cfg, 1) == 2 * cfg.out_h * cfg.out_w * 3 * 5 * 9
+
+
+def test_layer_config_validation():
+    with pytest.raises(ValueError):
+        wb.LayerConfig(N=0, C=1, H=4, W=4, K=1)
+    with pytest.raises(ValueError):
+        wb.LayerConfig(N=1, C=1, H=4, W=4, K=1, pad=-1)
+    with pytest.raises(ValueError):
+        wb.LayerConfig(N=1, C=1, H=2, W=2, K=1, pad=0)
+
+
+def test_forward_validation_errors_before_gpu():
+    """engine.py:211-218 error paths raise ValueError without touching the GPU."""
+    cfg = wb.LayerConfig(N=1, C=1, H=6, W=6, K=1, pad=1)
+    d32 = rand((1, 1, 6, 6), 1)
+    g64 = rand((1, 1, 3, 3), 2, wb.Precision.FP64)
+    with pytest.raises(ValueError):
+        wb.winograd_forward(d32, g64, cfg, wb.builtin(2, 3))
+    with pytest.raises(ValueError):
+        wb.winograd_forward(rand((1, 2, 6, 6), 1), rand((1, 1, 3, 3), 2), cfg)
+    cfg2 = wb.LayerConfig(N=1, C=1, H=6, W=6, K=1, R=2, S=2, pad=0)
+    with pytest.raises(ValueError):
+        wb.winograd_forward(rand((1, 1, 6, 6), 1), rand((1, 1, 2, 2), 2), cfg2, wb.builtin(2, 3))
+    with pytest.raises(ValueError):
+        wb.run_layer("f8x8", d32, rand((1, 1, 3, 3), 2), cfg)
+
+
+def test_plan_info_and_planner():
+    cfg = wb.LayerConfig(N=1, C=64, H=56, W=56, K=64, pad=1)
+    p = wb.WinogradPlan(cfg, 2, "fp32")
+    i = p.info
+    assert (i["tiles_h"], i["tiles_w"], i["P"], i["alpha"]) == (28, 28, 784, 4)
+    assert i["multiplies"] == wb.multiply_stage_flops(cfg, 2)
+    assert i["op_splits"] == 2 and i["op_bytes"] == 4 and i["num_chunks"] == 1
+    # the chunk planner respects the workspace budget with whole tile rows
+    big = wb.LayerConfig(N=64, C=64, H=224, W=224, K=64, pad=1)
+    for m, prec in ((4, "bf16"), (2, "fp32")):
+        q = wb.WinogradPlan(big, m, prec, workspace_limit=32 << 20)
+        j = q.info
+        per_tile = j["op_splits"] * j["op_bytes"] * (m + 2) ** 2 * j["c_pad"] + (m + 2) ** 2 * 64 * 4
+        assert j["chunk_tiles"] % j["tiles_w"] == 0
+        assert j["chunk_tiles"] * per_tile <= 32 << 20
+        assert j["num_chunks"] * j["rows_per_chunk"] >= 64 * j["tiles_h"]
+        assert j["launches_per_forward"] == 3 * j["num_chunks"]
+
+
+def test_plan_errors_map_to_reference_exceptions():
+    with pytest.raises(ValueError):
+        wb.WinogradPlan(wb.LayerConfig(N=1, C=1, H=6, W=6, K=1, pad=1), 3, "fp32")
+    with pytest.raises(ValueError):
+        wb.WinogradPlan(wb.LayerConfig(N=1, C=1, H=6, W=6, K=1, pad=1), 2, "int8")
+    with pytest.raises(ValueError):
+        wb.WinogradPlan(wb.LayerConfig(N=1, C=1, H=6, W=6, K=1, R=5, S=5, pad=2), 2, "fp32")
+
+
+def test_parse_algo():
+    assert wb.parse_algo("f2x2") == (2, False, None)
+    assert wb.parse_algo("f4x4-fx:bf16") == (4, True, "bf16")
+    with pytest.raises(ValueError):
+        wb.parse_algo("fft")
+    with pytest.raises(ValueError):
+        wb.parse_algo("f4x4:int4")
+
+
+def test_suites():
+    s = wb.vgg_e()
+    assert len(s.entries) == 9 and round(s.total_gflops_direct(), 2) == 39.02
+    assert sum(e.cfg.depth for e in s.entries) == 16
+    sc = s.scaled(0.05)
+    assert all(e.cfg.H >= 3 for e in sc.entries)
+    assert all(e.cfg.N == 8 for e in s.with_batch(8).entries)
+    assert wb.get_suite("vgg-e-accuracy").labels() == ("conv1.2", "conv2.2", "conv3.2",
+                                                        "conv4.2", "conv5")
+
+
+def test_counter():
+    c = wb.OpCounter()
+    c.add("mul", 3)
+    c.add("mul", 4)
+    assert c["mul"] == 7 and c.get("cmul") == 0
+    with pytest.raises(ValueError):
+        c.add("mul", -1)
+
+
+@pytest.mark.parametrize("N,world", [(64, 8), (64, 3), (5, 8), (1, 1), (7, 2)])
+def test_shard_bounds_partition(N, world):
+    spans = [sharding.shard_bounds(N, world, r) for r in range(world)]
+    assert sum(c for _, c in spans) == N
+    pos = 0
+    for s, c in spans:
+        assert s == pos
+        pos += c
+    assert max(c for _, c in spans) - min(c for _, c in spans) <= 1
+
+
+def test_filter_cache_key_semantics():
+    g = rand((2, 3, 3, 3), 1)
+    alg = wb.builtin(4, 3)
+    k1 = engine.FilterCache._key(g, alg, "fp32")
+    assert k1 == engine.FilterCache._key(rand((2, 3, 3, 3), 1), alg, "fp32")
+    assert k1 != engine.FilterCache._key(rand((2, 3, 3, 3), 2), alg, "fp32")
+    assert k1 != engine.FilterCache._key(g, alg, "bf16")
+    assert k1 != engine.FilterCache._key(g, wb.builtin(2, 3), "fp32")
