@@ -334,21 +334,19 @@ def run_gpu(args) -> None:
     images_per_s = B * world * args.steps / t_max
 
     # ---- live per-stage kernel timing (CUDA events on the launch stream)
-    stage_ms = [0.0] * 4
-    stage_n = [0] * 4
     stage_bytes = [0.0] * 4  # algorithmic HBM bytes
     stage_flops = [0.0] * 4
+    timer = weng.StageTimer()
     for L in layers:
         c, info = L["cfg"], L["plan"].info
         a2 = info["alpha"] ** 2
         es, ns = info["op_bytes"], info["op_splits"]
         for _ in range(L["depth"]):
-            flush.fill_(1)
-            ms, n = L["plan"].forward_timed(L["d"], L["y"], U=L["U"], g=None if fx else L["g"],
-                                            workspace=L["ws"], stream=stream)
-            for j in range(4):
-                stage_ms[j] += ms[j]
-                stage_n[j] += n[j]
+            with torch.cuda.stream(stream):
+                flush.fill_(1)  # also gives the host a head start: no launch gaps timed
+            timer.gap()
+            L["plan"].forward_timed(L["d"], L["y"], timer, U=L["U"], g=None if fx else L["g"],
+                                    workspace=L["ws"], stream=stream)
             P, C, K = info["P"], c.C, c.K
             if not fx:
                 stage_bytes[0] += 4 * 9 * K * C + ns * es * a2 * K * C
@@ -356,6 +354,7 @@ def run_gpu(args) -> None:
             stage_bytes[2] += ns * es * a2 * (C * P + K * C) + 4 * a2 * K * P
             stage_bytes[3] += 4 * a2 * K * P + 4 * c.N * K * c.out_h * c.out_w
             stage_flops[2] += 2.0 * a2 * K * C * P * (3 if prec == "fp32" else 1)
+    stage_ms, stage_n = timer.read()
     hbm_peak, bf16_peak, peak_src = load_peaks()
     tensor_peak = bf16_peak if prec in ("bf16", "fp16") else bf16_peak / 2  # tf32 = bf16/2
     dom = max(range(4), key=lambda j: stage_ms[j])

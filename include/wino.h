@@ -62,6 +62,7 @@ typedef struct {
   long long P;                /* N * tiles_h * tiles_w  (engine.py:67-69)        */
   int prec, c_pad, op_bytes, op_splits;
   int gemm_bn;                /* filters per GEMM CTA (tcgen05 N)                */
+  int gemm_splits;            /* split-C factor of the GEMM (small-P layers)     */
   int rows_per_chunk;         /* tile rows per workspace chunk                   */
   int num_chunks;
   long long chunk_tiles;      /* tiles per full chunk                            */
@@ -101,14 +102,20 @@ int wino_forward_host(wino_plan_t plan, const void* d_host, const void* U, const
                       void* y_host, void* d_dev, void* y_dev, void* workspace,
                       size_t workspace_bytes, void* stream);
 
-/* wino_forward with CUDA events recorded on `stream` between the pipeline
- * stages; synchronises the stream and ADDS each stage's device time (ms) to
- * stage_ms[0..3] = {filter transform, input transform, GEMM, output
- * transform} and its launch count to launches[0..3].  Used by bench.py to
- * measure the dominant kernel live; not for production calls. */
+/* Stage timer (diagnostics / bench): wino_forward_timed enqueues the same
+ * forward plus one CUDA event after every launch on `stream`, without any host
+ * synchronisation.  wino_timer_read synchronises on the last event and ADDS
+ * each stage's device time (ms) to stage_ms[0..3] = {filter transform, input
+ * transform, GEMM, output transform} and its launch count to launches[0..3],
+ * then resets the timer.  wino_timer_break marks a gap (e.g. an unrelated
+ * kernel enqueued between two timed forwards) so it is not attributed. */
+typedef struct wino_timer_s* wino_timer_t;
+int wino_timer_create(wino_timer_t* out);
+int wino_timer_destroy(wino_timer_t timer);
+int wino_timer_break(wino_timer_t timer);
+int wino_timer_read(wino_timer_t timer, float* stage_ms, int* launches);
 int wino_forward_timed(wino_plan_t plan, const void* d, const void* U, const void* g, void* y,
-                       void* workspace, size_t workspace_bytes, void* stream, float* stage_ms,
-                       int* launches);
+                       void* workspace, size_t workspace_bytes, void* stream, wino_timer_t timer);
 
 /* Last error message of the calling thread ("" if none). */
 const char* wino_last_error(void);

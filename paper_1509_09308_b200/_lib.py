@@ -23,6 +23,7 @@ PREC_NAME = {PREC_FP32: "fp32", PREC_TF32: "tf32", PREC_BF16: "bf16",
 # Every symbol include/wino.h declares (checked by tests/test_abi.py).
 EXPORTED = ("wino_plan_create", "wino_plan_destroy", "wino_plan_get_info",
             "wino_filter_transform", "wino_forward", "wino_forward_host", "wino_forward_timed",
+            "wino_timer_create", "wino_timer_destroy", "wino_timer_break", "wino_timer_read",
             "wino_last_error", "wino_version")
 
 
@@ -40,7 +41,7 @@ class PlanInfo(ctypes.Structure):
         ("P", ctypes.c_longlong),
         ("prec", ctypes.c_int), ("c_pad", ctypes.c_int), ("op_bytes", ctypes.c_int),
         ("op_splits", ctypes.c_int),
-        ("gemm_bn", ctypes.c_int),
+        ("gemm_bn", ctypes.c_int), ("gemm_splits", ctypes.c_int),
         ("rows_per_chunk", ctypes.c_int), ("num_chunks", ctypes.c_int),
         ("chunk_tiles", ctypes.c_longlong),
         ("u_bytes", ctypes.c_size_t), ("workspace_bytes", ctypes.c_size_t),
@@ -67,8 +68,11 @@ def _load() -> ctypes.CDLL:
     lib.wino_filter_transform.argtypes = [vp, vp, vp, vp]
     lib.wino_forward.argtypes = [vp, vp, vp, vp, vp, vp, sz, vp]
     lib.wino_forward_host.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
-    lib.wino_forward_timed.argtypes = [vp, vp, vp, vp, vp, vp, sz, vp,
-                                       ctypes.POINTER(ctypes.c_float), ctypes.POINTER(c_int)]
+    lib.wino_forward_timed.argtypes = [vp, vp, vp, vp, vp, vp, sz, vp, vp]
+    lib.wino_timer_create.argtypes = [ctypes.POINTER(vp)]
+    lib.wino_timer_destroy.argtypes = [vp]
+    lib.wino_timer_break.argtypes = [vp]
+    lib.wino_timer_read.argtypes = [vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(c_int)]
     lib.wino_last_error.restype = ctypes.c_char_p
     lib.wino_version.restype = ctypes.c_char_p
     for name in EXPORTED:

@@ -20,9 +20,10 @@ struct wino_plan_s {
   int oh, ow, th, tw;
   long long P;
   int c_pad, esize, nsplit, acc_bytes;
-  int bn;
+  int bn, splits;
   int rows_total, rows_per_chunk, num_chunks;
   long long chunk_tiles;
+  long long m_ld;                    // M row stride (tiles, multiple of 4)
   size_t u_bytes, v_bytes, m_bytes;  // v/m per full chunk
 };
 
@@ -69,10 +70,12 @@ bool encode_tmap_3d(void* map_out, int prec, const void* base, uint64_t d0, uint
   cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
   cuuint32_t box[3] = {box0, box1, 1};
   cuuint32_t estr[3] = {1, 1, 1};
+  // operand maps use the 128B swizzle UMMA expects; the accumulator store map
+  // (prec -1, fp32) is a plain row-major box
   CUresult r = g_encode(reinterpret_cast<CUtensorMap*>(map_out), dt, 3, const_cast<void*>(base),
                         dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        prec < 0 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (%d): dims %llu,%llu,%llu strides %llu,%llu", (int)r,
               (unsigned long long)d0, (unsigned long long)d1, (unsigned long long)d2,
@@ -185,10 +188,27 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
   p->rows_per_chunk = static_cast<int>(rows);
   p->num_chunks = (p->rows_total + p->rows_per_chunk - 1) / p->rows_per_chunk;
   p->chunk_tiles = static_cast<long long>(p->rows_per_chunk) * p->tw;
+
+  // ---- split-C for small-P layers (single chunk): enough GEMM work units to
+  // cover the SMs; partial sums land in separate M slices.
+  p->splits = 1;
+  if (prec != kFP64 && p->num_chunks == 1) {
+    const int sms = gemm_device_sms();
+    const int num_kb = gemm_num_kblocks(prec, L.C);
+    const long long units = ((p->chunk_tiles + 127) / 128) * ((L.K + p->bn - 1) / p->bn) * p->a2;
+    if (units < sms && num_kb > 1) {
+      int sp = static_cast<int>((sms + units - 1) / units);
+      if (sp > num_kb) sp = num_kb;
+      const int kbps = (num_kb + sp - 1) / sp;
+      p->splits = (num_kb + kbps - 1) / kbps;
+    }
+  }
   p->v_bytes = align_up(static_cast<size_t>(p->nsplit) * p->a2 * p->chunk_tiles * p->c_pad *
                             p->esize,
                         1024);
-  p->m_bytes = align_up(static_cast<size_t>(p->a2) * L.K * p->chunk_tiles * p->acc_bytes, 1024);
+  p->m_ld = static_cast<long long>(align_up(static_cast<size_t>(p->chunk_tiles), 4));
+  p->m_bytes = align_up(static_cast<size_t>(p->splits) * p->a2 * L.K * p->m_ld * p->acc_bytes,
+                        1024);
   *out = p;
   return WINO_OK;
 }
@@ -217,6 +237,7 @@ int wino_plan_get_info(wino_plan_t p, wino_plan_info_t* info) {
   info->op_bytes = p->esize;
   info->op_splits = p->nsplit;
   info->gemm_bn = p->bn;
+  info->gemm_splits = p->splits;
   info->rows_per_chunk = p->rows_per_chunk;
   info->num_chunks = p->num_chunks;
   info->chunk_tiles = p->chunk_tiles;
@@ -238,50 +259,46 @@ int wino_filter_transform(wino_plan_t p, const void* g, void* U, void* stream) {
   return e == cudaSuccess ? WINO_OK : cuda_fail(e, "filter transform");
 }
 
+// Stage timer: events recorded on the launch stream after every launch, read
+// back later (no host synchronisation inside the forward, so host launch
+// latency is not counted when the host runs ahead of the GPU).
+struct wino_timer_s {
+  static constexpr int kMax = 4096;
+  cudaEvent_t ev[kMax];
+  int stage[kMax];
+  int n = 0;
+  bool open = false;
+};
+
 namespace {
-struct StageTimer {  // optional per-stage CUDA-event timing on the launch stream
+struct StageTimer {
+  wino_timer_s* t;
   cudaStream_t s;
-  float* ms;
-  int* launches;
-  cudaEvent_t ev[2];
-  bool on;
-  StageTimer(cudaStream_t s_, float* ms_, int* l_) : s(s_), ms(ms_), launches(l_), on(ms_ != nullptr) {
-    if (on) {
-      cudaEventCreate(&ev[0]);
-      cudaEventCreate(&ev[1]);
+  StageTimer(cudaStream_t s_, wino_timer_s* t_) : t(t_), s(s_) {
+    if (t && !t->open && t->n < wino_timer_s::kMax) {  // opening event of a sequence
+      cudaEventRecord(t->ev[t->n], s);
+      t->stage[t->n++] = -1;
+      t->open = true;
     }
   }
-  ~StageTimer() {
-    if (on) {
-      cudaEventDestroy(ev[0]);
-      cudaEventDestroy(ev[1]);
-    }
-  }
-  void begin() {
-    if (on) cudaEventRecord(ev[0], s);
-  }
-  void end(int stage) {
-    if (!on) return;
-    cudaEventRecord(ev[1], s);
-    cudaEventSynchronize(ev[1]);
-    float t = 0.f;
-    cudaEventElapsedTime(&t, ev[0], ev[1]);
-    ms[stage] += t;
-    launches[stage] += 1;
+  void mark(int st) {
+    if (!t || t->n >= wino_timer_s::kMax) return;
+    cudaEventRecord(t->ev[t->n], s);
+    t->stage[t->n++] = st;
   }
 };
 }  // namespace
 
 static int forward_impl(wino_plan_t p, const void* d, const void* U, const void* g, void* y,
-                        void* workspace, size_t workspace_bytes, void* stream, float* stage_ms,
-                        int* launches) {
+                        void* workspace, size_t workspace_bytes, void* stream,
+                        wino_timer_s* timer) {
   g_err.clear();
   if (!p || !d || !y || (!U && !g) || !workspace) {
     set_error("null argument");
     return WINO_EINVAL;
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  StageTimer tm(s, stage_ms, launches);
+  StageTimer tm(s, timer);
   unsigned char* ws = static_cast<unsigned char*>(workspace);
   size_t need = p->v_bytes + p->m_bytes + (U ? 0 : p->u_bytes);
   if (workspace_bytes < need) {
@@ -289,10 +306,9 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
     return WINO_EINVAL;
   }
   if (!U) {
-    tm.begin();
     cudaError_t e = launch_filter_transform(p->m, p->prec, g, ws, p->L.K, p->L.C, p->c_pad, s);
     if (e != cudaSuccess) return cuda_fail(e, "filter transform");
-    tm.end(0);
+    tm.mark(0);
     U = ws;
     ws += p->u_bytes;
   }
@@ -304,41 +320,91 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
     const int rows = (row0 + p->rows_per_chunk <= p->rows_total) ? p->rows_per_chunk
                                                                   : p->rows_total - row0;
     const long long Pc = static_cast<long long>(rows) * p->tw;
-    tm.begin();
     cudaError_t e = launch_input_transform(p->m, p->prec, d, V, L.N, L.C, L.H, L.W, L.pad, p->th,
                                            p->tw, row0, rows, Pc, p->c_pad, s);
     if (e != cudaSuccess) return cuda_fail(e, "input transform");
-    tm.end(1);
-    GemmArgs ga{V, U, Mb, p->a2, L.K, L.C, p->c_pad, Pc, p->bn};
-    tm.begin();
+    tm.mark(1);
+    GemmArgs ga{V, U, Mb, p->a2, L.K, L.C, p->c_pad, Pc, p->bn, p->splits, p->m_ld};
     e = launch_batched_gemm(p->prec, ga, s);
     if (e != cudaSuccess) {
       if (g_err.empty()) return cuda_fail(e, "batched gemm");
       return WINO_ECUDA;
     }
-    tm.end(2);
-    tm.begin();
+    tm.mark(2);
     e = launch_output_transform(p->m, p->prec, Mb, y, L.N, L.K, p->th, p->tw, p->oh, p->ow, row0,
-                                Pc, s);
+                                Pc, p->m_ld, p->splits, s);
     if (e != cudaSuccess) return cuda_fail(e, "output transform");
-    tm.end(3);
+    tm.mark(3);
   }
   return WINO_OK;
 }
 
 int wino_forward(wino_plan_t p, const void* d, const void* U, const void* g, void* y,
                  void* workspace, size_t workspace_bytes, void* stream) {
-  return forward_impl(p, d, U, g, y, workspace, workspace_bytes, stream, nullptr, nullptr);
+  return forward_impl(p, d, U, g, y, workspace, workspace_bytes, stream, nullptr);
 }
 
-int wino_forward_timed(wino_plan_t p, const void* d, const void* U, const void* g, void* y,
-                       void* workspace, size_t workspace_bytes, void* stream, float* stage_ms,
-                       int* launches) {
-  if (!stage_ms || !launches) {
+int wino_timer_create(wino_timer_t* out) {
+  if (!out) {
     set_error("null argument");
     return WINO_EINVAL;
   }
-  return forward_impl(p, d, U, g, y, workspace, workspace_bytes, stream, stage_ms, launches);
+  wino_timer_s* t = new (std::nothrow) wino_timer_s();
+  if (!t) return WINO_ENOMEM;
+  for (int i = 0; i < wino_timer_s::kMax; ++i) {
+    cudaError_t e = cudaEventCreate(&t->ev[i]);
+    if (e != cudaSuccess) {
+      for (int j = 0; j < i; ++j) cudaEventDestroy(t->ev[j]);
+      delete t;
+      return cuda_fail(e, "timer events");
+    }
+  }
+  *out = t;
+  return WINO_OK;
+}
+
+int wino_timer_destroy(wino_timer_t t) {
+  if (t) {
+    for (int i = 0; i < wino_timer_s::kMax; ++i) cudaEventDestroy(t->ev[i]);
+    delete t;
+  }
+  return WINO_OK;
+}
+
+int wino_timer_break(wino_timer_t t) {
+  if (!t) return WINO_EINVAL;
+  t->open = false;  // the next timed forward starts a new sequence
+  return WINO_OK;
+}
+
+int wino_timer_read(wino_timer_t t, float* stage_ms, int* launches) {
+  if (!t || !stage_ms || !launches) {
+    set_error("null argument");
+    return WINO_EINVAL;
+  }
+  if (t->n > 0) {
+    cudaError_t e = cudaEventSynchronize(t->ev[t->n - 1]);
+    if (e != cudaSuccess) return cuda_fail(e, "timer sync");
+  }
+  for (int i = 1; i < t->n; ++i) {
+    if (t->stage[i] < 0) continue;  // sequence opener
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t->ev[i - 1], t->ev[i]);
+    stage_ms[t->stage[i]] += ms;
+    launches[t->stage[i]] += 1;
+  }
+  t->n = 0;
+  t->open = false;
+  return WINO_OK;
+}
+
+int wino_forward_timed(wino_plan_t p, const void* d, const void* U, const void* g, void* y,
+                       void* workspace, size_t workspace_bytes, void* stream, wino_timer_t timer) {
+  if (!timer) {
+    set_error("null timer");
+    return WINO_EINVAL;
+  }
+  return forward_impl(p, d, U, g, y, workspace, workspace_bytes, stream, timer);
 }
 
 int wino_forward_host(wino_plan_t p, const void* d_host, const void* U, const void* g,

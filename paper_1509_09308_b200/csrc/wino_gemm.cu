@@ -2,11 +2,14 @@
 //   M[comp][k][p] = sum_c U[comp][k][c] * V[comp][p][c]
 // (reference: batched_matmul -> _bgemm, kernels.py:31-65; engine.py:239).
 //
-// sm_100a tensor-core kernel: one CTA computes a 128-tile x BN-filter block of
-// one component.  Warp-specialised:
+// sm_100a tensor-core kernel, persistent: each CTA strides through work units
+// (one 128-tile x BN-filter block of one component, optionally one split of
+// the channel reduction).  Warp-specialised:
 //   warp 0   : TMA producer (one elected lane), STAGES-deep mbarrier ring
 //   warp 1   : TMEM allocator + single-thread tcgen05.mma issuer
 //   warps 2-5: epilogue, tcgen05.ld TMEM -> registers -> coalesced fp32 stores
+// TMEM holds two BN-column accumulators so the epilogue of one unit overlaps
+// the MMAs of the next.
 // Operands are K-major (channels contiguous) in the 128-byte-swizzle canonical
 // layout the TMA box writes; the accumulator (128 lanes x BN fp32 columns)
 // lives in TMEM.  The MMA M dimension runs over tiles P (so a warp's epilogue
@@ -38,21 +41,33 @@ struct GemmTraits {
   static constexpr uint32_t fmt = (PREC == kBF16) ? 1u : (PREC == kFP16 ? 0u : 2u);
 };
 
+constexpr int kEpiWarps = 4;
+constexpr int kEpiBuf = 32 * 32 * 4;  // one 32-tile x 32-filter fp32 block
+
 template <int PREC, int BN>
 struct GemmSmem {
   using Tr = GemmTraits<PREC>;
   static constexpr int a_bytes = kTileP * 128;  // 128 rows x 128 B
   static constexpr int b_bytes = BN * 128;
   static constexpr int stage_bytes = Tr::nsplit * (a_bytes + b_bytes);
-  static constexpr int stages = (200 * 1024) / stage_bytes >= 6 ? 6 : (200 * 1024) / stage_bytes;
-  static constexpr int bar_offset = stages * stage_bytes;
+  static constexpr int epi_bytes = kEpiWarps * 2 * kEpiBuf;  // double-buffered per warp
+  static constexpr int avail = 227 * 1024 - 1024 - 256 - epi_bytes;
+  static constexpr int stages = avail / stage_bytes >= 6 ? 6 : avail / stage_bytes;
+  static constexpr int epi_offset = stages * stage_bytes;
+  static constexpr int bar_offset = epi_offset + epi_bytes;
   static constexpr int total = bar_offset + 256 + 1024;  // barriers + alignment slack
 };
 
+// Persistent, warp-specialised tcgen05 GEMM.  Work unit = (split, comp,
+// filter block, tile block); CTAs stride through units.  The accumulator is
+// double-buffered in TMEM (2 x BN columns) so the epilogue of unit j overlaps
+// the MMAs of unit j+1.  Split-C units (small-P layers) write partial sums to
+// separate M slices that the output transform adds in a fixed order.
 template <int PREC, int BN>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     wgemm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmU,
-                    float* __restrict__ Mout, int K, long long Pc, int num_kb, int a2) {
+                    const __grid_constant__ CUtensorMap tmM, int a2, int num_kb,
+                    int kb_per_split, int n_pblk, int n_kblk, int n_units) {
   using Tr = GemmTraits<PREC>;
   using Sm = GemmSmem<PREC, BN>;
   constexpr int STAGES = Sm::stages;
@@ -60,49 +75,67 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
 
   extern __shared__ unsigned char smem_raw[];
-  // 1024-byte alignment for the 128B swizzle atoms
   unsigned char* smem = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Sm::bar_offset);
   uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tfull = empty + STAGES;   // [2] accumulator ready
+  uint64_t* tempty = tfull + 2;       // [2] accumulator drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int p0 = blockIdx.x * kTileP;
-  const int k0 = blockIdx.y * BN;
-  const int comp = blockIdx.z;
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmV);
     ptx::prefetch_tmap(&tmU);
+    ptx::prefetch_tmap(&tmM);
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
     }
-    ptx::mbar_init(tmem_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&tfull[b], 1);
+      ptx::mbar_init(&tempty[b], 128);
+    }
     ptx::fence_mbar_init();
   }
-  if (warp == 1) ptx::tmem_alloc(tmem_slot, BN);
+  if (warp == 1) ptx::tmem_alloc(tmem_slot, 2 * BN);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  auto decode = [&](int u, int& pb, int& kbk, int& comp, int& split) {
+    pb = u % n_pblk;
+    int r = u / n_pblk;
+    kbk = r % n_kblk;
+    r /= n_kblk;
+    comp = r % a2;
+    split = r / a2;
+  };
+
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
-      for (int kb = 0; kb < num_kb; ++kb) {
-        const int s = kb % STAGES;
-        if (kb >= STAGES) ptx::mbar_wait(&empty[s], ((kb / STAGES) - 1) & 1);
-        unsigned char* st = smem + s * Sm::stage_bytes;
-        ptx::mbar_arrive_expect_tx(&full[s], Sm::stage_bytes);
+      int it = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        int pb, kbk, comp, split;
+        decode(u, pb, kbk, comp, split);
+        const int kb0 = split * kb_per_split;
+        const int kb1 = min(num_kb, kb0 + kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % STAGES;
+          ptx::mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+          unsigned char* st = smem + s * Sm::stage_bytes;
+          ptx::mbar_arrive_expect_tx(&full[s], Sm::stage_bytes);
 #pragma unroll
-        for (int h = 0; h < Tr::nsplit; ++h) {
-          ptx::tma_load_3d(st + h * Sm::a_bytes, &tmV, &full[s], kb * Tr::bk, p0, comp + h * a2);
-          ptx::tma_load_3d(st + Tr::nsplit * Sm::a_bytes + h * Sm::b_bytes, &tmU, &full[s],
-                           kb * Tr::bk, k0, comp + h * a2);
+          for (int h = 0; h < Tr::nsplit; ++h) {
+            ptx::tma_load_3d(st + h * Sm::a_bytes, &tmV, &full[s], kb * Tr::bk, pb * kTileP,
+                             comp + h * a2);
+            ptx::tma_load_3d(st + Tr::nsplit * Sm::a_bytes + h * Sm::b_bytes, &tmU, &full[s],
+                             kb * Tr::bk, kbk * BN, comp + h * a2);
+          }
         }
       }
     }
@@ -110,58 +143,89 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = ptx::umma_idesc(Tr::fmt, kTileP, BN);
-      for (int kb = 0; kb < num_kb; ++kb) {
-        const int s = kb % STAGES;
-        ptx::mbar_wait(&full[s], (kb / STAGES) & 1);
+      int it = 0, j = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++j) {
+        int pb, kbk, comp, split;
+        decode(u, pb, kbk, comp, split);
+        const int kb0 = split * kb_per_split;
+        const int kb1 = min(num_kb, kb0 + kb_per_split);
+        const int acc = j & 1;
+        ptx::mbar_wait(&tempty[acc], ((j >> 1) & 1) ^ 1);
         ptx::tc_fence_after();
-        const uint32_t st = ptx::smem_u32(smem + s * Sm::stage_bytes);
-        const uint32_t a_hi = st, a_lo = st + Sm::a_bytes;
-        const uint32_t b_hi = st + Tr::nsplit * Sm::a_bytes;
-        const uint32_t b_lo = b_hi + Sm::b_bytes;
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % STAGES;
+          ptx::mbar_wait(&full[s], (it / STAGES) & 1);
+          ptx::tc_fence_after();
+          const uint32_t st = ptx::smem_u32(smem + s * Sm::stage_bytes);
+          const uint32_t a_hi = st, a_lo = st + Sm::a_bytes;
+          const uint32_t b_hi = st + Tr::nsplit * Sm::a_bytes;
+          const uint32_t b_lo = b_hi + Sm::b_bytes;
 #pragma unroll
-        for (int k = 0; k < Tr::bk / Tr::uk; ++k) {
-          const uint32_t off = k * 32;  // 32 bytes of K per MMA inside the swizzle atom
-          const uint32_t acc = (kb | k) ? 1u : 0u;
-          if constexpr (Tr::nsplit == 2) {
-            ptx::umma<1>(tmem_base, ptx::umma_desc_sw128(a_lo + off),
-                         ptx::umma_desc_sw128(b_hi + off), idesc, acc);
-            ptx::umma<1>(tmem_base, ptx::umma_desc_sw128(a_hi + off),
-                         ptx::umma_desc_sw128(b_lo + off), idesc, 1u);
-            ptx::umma<1>(tmem_base, ptx::umma_desc_sw128(a_hi + off),
-                         ptx::umma_desc_sw128(b_hi + off), idesc, 1u);
-          } else {
-            ptx::umma<Tr::kind>(tmem_base, ptx::umma_desc_sw128(a_hi + off),
-                                ptx::umma_desc_sw128(b_hi + off), idesc, acc);
+          for (int k = 0; k < Tr::bk / Tr::uk; ++k) {
+            const uint32_t off = k * 32;  // 32 bytes of K per MMA inside the swizzle atom
+            const uint32_t accum = (kb != kb0 || k != 0) ? 1u : 0u;
+            if constexpr (Tr::nsplit == 2) {
+              ptx::umma<1>(d_tmem, ptx::umma_desc_sw128(a_lo + off),
+                           ptx::umma_desc_sw128(b_hi + off), idesc, accum);
+              ptx::umma<1>(d_tmem, ptx::umma_desc_sw128(a_hi + off),
+                           ptx::umma_desc_sw128(b_lo + off), idesc, 1u);
+              ptx::umma<1>(d_tmem, ptx::umma_desc_sw128(a_hi + off),
+                           ptx::umma_desc_sw128(b_hi + off), idesc, 1u);
+            } else {
+              ptx::umma<Tr::kind>(d_tmem, ptx::umma_desc_sw128(a_hi + off),
+                                  ptx::umma_desc_sw128(b_hi + off), idesc, accum);
+            }
           }
+          ptx::umma_commit(&empty[s]);  // frees the smem slot when these MMAs retire
         }
-        ptx::umma_commit(&empty[s]);  // frees the smem slot when these MMAs retire
+        ptx::umma_commit(&tfull[acc]);  // accumulator complete
       }
-      ptx::umma_commit(tmem_full);    // accumulator complete
     }
   } else {
     // ------------------------------------------------------------ epilogue
+    // TMEM -> registers -> smem [32 filters][32 tiles] -> TMA bulk store into
+    // M[split*a2 + comp][k][p]; the tensor map clips tiles >= Pc / filters >= K.
     const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const long long p = p0 + q * 32 + lane;
-    ptx::mbar_wait(tmem_full, 0);
-    ptx::tc_fence_after();
-    float* mrow = Mout + static_cast<size_t>(comp) * K * Pc;
+    float* buf0 = reinterpret_cast<float*>(smem + Sm::epi_offset + (warp - 2) * 2 * kEpiBuf);
+    int j = 0, nbuf = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++j) {
+      int pb, kbk, comp, split;
+      decode(u, pb, kbk, comp, split);
+      const int acc = j & 1;
+      ptx::mbar_wait(&tfull[acc], (j >> 1) & 1);
+      ptx::tc_fence_after();
+      const int p0 = pb * kTileP + q * 32;
+      const int z = split * a2 + comp;
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      uint32_t r[32];
-      ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + c0, r);
-      ptx::tmem_ld_wait();
-      if (p < Pc) {
+      for (int c0 = 0; c0 < BN; c0 += 32, ++nbuf) {
+        uint32_t r[32];
+        ptx::tmem_ld_32x32b_x32(tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16) + c0,
+                                r);
+        float* buf = buf0 + (nbuf & 1) * (kEpiBuf / 4);
+        if (lane == 0) ptx::bulk_wait_read<1>();  // the store that last used `buf` has read it
+        __syncwarp();
+        ptx::tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int k = k0 + c0 + j;
-          if (k < K) mrow[static_cast<size_t>(k) * Pc + p] = __uint_as_float(r[j]);
+        for (int jj = 0; jj < 32; ++jj) buf[jj * 32 + lane] = __uint_as_float(r[jj]);
+        ptx::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          ptx::tma_store_3d(&tmM, buf, p0, kbk * BN + c0, z);
+          ptx::bulk_commit();
         }
       }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&tempty[acc]);
     }
+    if (lane == 0) ptx::bulk_wait_all();
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 1) ptx::tmem_dealloc(tmem_base, BN);
+  if (warp == 1) {
+    __syncwarp();
+    ptx::tmem_dealloc(tmem_base, 2 * BN);
+  }
 }
 
 // ------------------------------------------------------------ fp64 CUDA-core
@@ -170,7 +234,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 __global__ void __launch_bounds__(256) wgemm_f64_kernel(const double* __restrict__ V,
                                                         const double* __restrict__ U,
                                                         double* __restrict__ Mout, int K,
-                                                        long long Pc, int C, int c_pad) {
+                                                        long long Pc, int C, int c_pad,
+                                                        long long m_ld) {
   __shared__ double sv[16][65];
   __shared__ double su[16][65];
   const int comp = blockIdx.z;
@@ -204,7 +269,7 @@ __global__ void __launch_bounds__(256) wgemm_f64_kernel(const double* __restrict
     }
     __syncthreads();
   }
-  double* Mc = Mout + static_cast<size_t>(comp) * K * Pc;
+  double* Mc = Mout + static_cast<size_t>(comp) * K * m_ld;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int k = k0 + ty * 4 + i;
@@ -212,12 +277,23 @@ __global__ void __launch_bounds__(256) wgemm_f64_kernel(const double* __restrict
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const long long p = p0 + tx * 4 + j;
-      if (p < Pc) Mc[static_cast<size_t>(k) * Pc + p] = acc[i][j];
+      if (p < Pc) Mc[static_cast<size_t>(k) * m_ld + p] = acc[i][j];
     }
   }
 }
 
 // ------------------------------------------------------------ launch
+static int num_sms() {
+  static int n = 0;  // benign race: idempotent
+  if (n == 0) {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    n = v > 0 ? v : 148;
+  }
+  return n;
+}
+
 template <int PREC, int BN>
 static cudaError_t launch_tc(const GemmArgs& a, cudaStream_t s) {
   using Tr = GemmTraits<PREC>;
@@ -231,20 +307,39 @@ static cudaError_t launch_tc(const GemmArgs& a, cudaStream_t s) {
   if (!encode_tmap_3d(&tmU, PREC, a.U, a.C, a.K, planes, a.c_pad * es,
                       static_cast<uint64_t>(a.K) * a.c_pad * es, Tr::bk, BN))
     return cudaErrorInvalidValue;
+  const int splits = a.splits < 1 ? 1 : a.splits;
+  alignas(64) CUtensorMap tmM;
+  if (!encode_tmap_3d(&tmM, -1, a.M, a.Pc, a.K, static_cast<uint64_t>(splits) * a.a2,
+                      a.m_ld * 4ull, static_cast<uint64_t>(a.K) * a.m_ld * 4ull, 32, 32))
+    return cudaErrorInvalidValue;
   auto kern = wgemm_tc_kernel<PREC, BN>;
   static bool configured = false;  // idempotent attribute set
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Sm::total);
     if (e != cudaSuccess) return e;
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
     configured = true;
   }
   const int num_kb = (a.C + Tr::bk - 1) / Tr::bk;
-  const dim3 grid(static_cast<unsigned>((a.Pc + kTileP - 1) / kTileP), (a.K + BN - 1) / BN, a.a2);
-  kern<<<grid, kGemmThreads, Sm::total, s>>>(tmV, tmU, static_cast<float*>(a.M), a.K, a.Pc,
-                                             num_kb, a.a2);
+  const int kbps = (num_kb + splits - 1) / splits;
+  const int n_pblk = static_cast<int>((a.Pc + kTileP - 1) / kTileP);
+  const int n_kblk = (a.K + BN - 1) / BN;
+  const long long units = static_cast<long long>(n_pblk) * n_kblk * a.a2 * splits;
+  if (units > 0x7fffffffLL) return cudaErrorInvalidValue;
+  const int grid = static_cast<int>(units < num_sms() ? units : num_sms());
+  kern<<<grid, kGemmThreads, Sm::total, s>>>(tmV, tmU, tmM, a.a2, num_kb, kbps, n_pblk, n_kblk,
+                                             static_cast<int>(units));
   return cudaGetLastError();
 }
+
+int gemm_num_kblocks(int prec, int C) {
+  const int bk = (prec == kBF16 || prec == kFP16) ? 64 : 32;
+  return (C + bk - 1) / bk;
+}
+
+int gemm_device_sms() { return num_sms(); }
 
 template <int PREC>
 static cudaError_t launch_prec(const GemmArgs& a, cudaStream_t s) {
@@ -268,7 +363,8 @@ cudaError_t launch_batched_gemm(int prec, const GemmArgs& a, cudaStream_t s) {
       const dim3 grid(static_cast<unsigned>((a.Pc + 63) / 64), (a.K + 63) / 64, a.a2);
       wgemm_f64_kernel<<<grid, 256, 0, s>>>(static_cast<const double*>(a.V),
                                             static_cast<const double*>(a.U),
-                                            static_cast<double*>(a.M), a.K, a.Pc, a.C, a.c_pad);
+                                            static_cast<double*>(a.M), a.K, a.Pc, a.C, a.c_pad,
+                                            a.m_ld);
       return cudaGetLastError();
     }
     default: return cudaErrorInvalidValue;

@@ -39,19 +39,24 @@ cudaError_t launch_input_transform(int m, int prec, const void* d, void* V, int 
                                    int W, int pad, int th, int tw, int row0, int rows,
                                    long long Pc, int c_pad, cudaStream_t s);
 
-// M [alpha^2][K][Pc] (float, or double for FP64) -> y (N,K,oh,ow), clipped
+// M [splits][alpha^2][K][m_ld] (float, or double for FP64) -> y (N,K,oh,ow), clipped;
+// split slices are summed in ascending order (deterministic).
 cudaError_t launch_output_transform(int m, int prec, const void* Mbuf, void* y, int N, int K,
                                     int th, int tw, int oh, int ow, int row0, long long Pc,
-                                    cudaStream_t s);
+                                    long long m_ld, int splits, cudaStream_t s);
 
 struct GemmArgs {
   const void* V;   // [nsplit][a2][Pc][c_pad]
   const void* U;   // [nsplit][a2][K][c_pad]
-  void* M;         // [a2][K][Pc]
+  void* M;         // [splits][a2][K][Pc]
   int a2, K, C, c_pad;
   long long Pc;
   int bn;          // filters per CTA (tcgen05 N)
+  int splits;      // split-C factor: partial sums go to M slices [splits][a2][K][m_ld]
+  long long m_ld;  // M row stride (>= Pc, multiple of 4 for the TMA store)
 };
+int gemm_num_kblocks(int prec, int C);
+int gemm_device_sms();
 // Tensor-core (tcgen05) GEMM for FP32/TF32/BF16/FP16, CUDA-core fp64 for FP64.
 cudaError_t launch_batched_gemm(int prec, const GemmArgs& a, cudaStream_t s);
 int gemm_kernels_per_launch(int prec);

@@ -117,7 +117,7 @@ class WinogradPlan:
 
     def __del__(self) -> None:
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and _lib is not None and _lib.lib is not None:
             _lib.lib.wino_plan_destroy(h)
             self._h = None
 
@@ -183,17 +183,15 @@ class WinogradPlan:
             workspace.data_ptr(), workspace.numel(), _stream_handle(stream)), "wino_forward")
         return y
 
-    def forward_timed(self, d, y, U=None, g=None, workspace=None, stream=None):
-        """forward() with per-stage CUDA-event timing (synchronising).  Returns
-        (stage_ms[4], launches[4]) for {filter, input, gemm, output}."""
-        ms = (ctypes.c_float * 4)()
-        n = (ctypes.c_int * 4)()
+    def forward_timed(self, d, y, timer: "StageTimer", U=None, g=None, workspace=None,
+                      stream=None):
+        """forward() plus one CUDA event per launch into `timer` (asynchronous)."""
         _lib.check(_lib.lib.wino_forward_timed(
             self._h, d.data_ptr(), U.data_ptr() if U is not None else None,
             g.data_ptr() if g is not None and U is None else None, y.data_ptr(),
-            workspace.data_ptr(), workspace.numel(), _stream_handle(stream), ms, n),
+            workspace.data_ptr(), workspace.numel(), _stream_handle(stream), timer._h),
             "wino_forward_timed")
-        return list(ms), list(n)
+        return y
 
     def forward_host(self, d_host, y_host, d_dev, y_dev, U=None, g=None, workspace=None,
                      stream=None):
@@ -204,6 +202,33 @@ class WinogradPlan:
             d_dev.data_ptr(), y_dev.data_ptr(), workspace.data_ptr(), workspace.numel(),
             _stream_handle(stream)), "wino_forward_host")
         return y_host
+
+
+class StageTimer:
+    """Device-side per-stage timing of forwards (wino_timer_t)."""
+
+    STAGES = ("filter_transform", "input_transform", "batched_gemm", "output_transform")
+
+    def __init__(self) -> None:
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib.wino_timer_create(ctypes.byref(h)), "wino_timer_create")
+        self._h = h
+
+    def gap(self) -> None:
+        _lib.check(_lib.lib.wino_timer_break(self._h))
+
+    def read(self):
+        """Synchronise; returns (stage_ms[4], launches[4]) accumulated since last read."""
+        ms = (ctypes.c_float * 4)()
+        n = (ctypes.c_int * 4)()
+        _lib.check(_lib.lib.wino_timer_read(self._h, ms, n), "wino_timer_read")
+        return list(ms), list(n)
+
+    def __del__(self) -> None:
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None and _lib.lib is not None:
+            _lib.lib.wino_timer_destroy(h)
+            self._h = None
 
 
 _plans: dict = {}

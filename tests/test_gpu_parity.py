@@ -169,3 +169,23 @@ def test_grad_inputs_matches_oracle(wb):
     flipped = np.ascontiguousarray(g[:, :, ::-1, ::-1].transpose(1, 0, 2, 3))
     ref = O.direct_forward(dy, flipped, 1)
     assert O.max_abs_error(out, ref) < 5e-3
+
+
+@pytest.mark.parametrize("m,prec", [(2, "fp32"), (4, "fp32"), (4, "bf16"), (2, "tf32")])
+def test_split_c_small_p_layer(wb, m, prec):
+    """conv5-like small-P layer: the planner splits the channel reduction across
+    CTAs; the output transform must re-assemble it exactly."""
+    import torch
+    cfg = wb.LayerConfig(N=1, C=512, H=14, W=14, K=256, pad=1)
+    plan = wb.WinogradPlan(cfg, m, prec)
+    assert plan.info["gemm_splits"] > 1
+    d = O.fill_uniform((1, 512, 14, 14), 31)
+    g = O.fill_uniform((256, 512, 3, 3), 32)
+    y = plan.forward(torch.from_numpy(d).cuda(), g=torch.from_numpy(g).cuda()).cpu().numpy()
+    ref = O.direct_forward(d, g, 1)
+    if prec == "fp32":
+        assert O.max_abs_error(y, ref) < (5e-4 if m == 2 else 5e-3)
+        yo = O.winograd_forward(d, g, m, 1)
+        assert np.abs(y - yo).max() <= 2e-5 * (1 + np.abs(yo).max())
+    else:
+        assert O.max_abs_error(y, ref) / np.abs(ref).max() <= REL_TOL[(prec, m)]
