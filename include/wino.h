@@ -69,6 +69,7 @@ typedef struct {
   size_t u_bytes;             /* transformed-filter stack U                      */
   size_t workspace_bytes;     /* V + M for one chunk (+ U when g is passed)      */
   int launches_per_forward;   /* kernels launched by one wino_forward (U given)  */
+  int fused_small_c;          /* 1: C <= 8, whole layer in one fused kernel      */
   long long multiplies;       /* P*C*K*alpha^2: the reference "mul" counter      */
 } wino_plan_info_t;
 

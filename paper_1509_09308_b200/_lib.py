@@ -45,7 +45,7 @@ class PlanInfo(ctypes.Structure):
         ("rows_per_chunk", ctypes.c_int), ("num_chunks", ctypes.c_int),
         ("chunk_tiles", ctypes.c_longlong),
         ("u_bytes", ctypes.c_size_t), ("workspace_bytes", ctypes.c_size_t),
-        ("launches_per_forward", ctypes.c_int),
+        ("launches_per_forward", ctypes.c_int), ("fused_small_c", ctypes.c_int),
         ("multiplies", ctypes.c_longlong),
     ]
 

@@ -7,6 +7,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -21,6 +22,7 @@ struct wino_plan_s {
   long long P;
   int c_pad, esize, nsplit, acc_bytes;
   int bn, splits;
+  bool smallc;  // whole layer in the fused tiny-C kernel (no V/M staging)
   int rows_total, rows_per_chunk, num_chunks;
   long long chunk_tiles;
   long long m_ld;                    // M row stride (tiles, multiple of 4)
@@ -83,6 +85,14 @@ bool encode_tmap_3d(void* map_out, int prec, const void* base, uint64_t d0, uint
     return false;
   }
   return true;
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("WINO_NO_PDL");
+    return !(v && v[0] == '1');
+  }();
+  return on;
 }
 
 static int cuda_fail(cudaError_t e, const char* what) {
@@ -176,6 +186,8 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
   while (bn > 64 && ptiles * ((L.K + bn - 1) / bn) * p->a2 < 148) bn /= 2;
   p->bn = bn;
 
+  p->smallc = L.C <= kSmallCMax;
+
   // ---- chunk planner: whole tile rows, V + M staging within the budget
   const size_t budget = workspace_limit ? workspace_limit : kDefaultWorkspace;
   const size_t per_tile = static_cast<size_t>(p->nsplit) * p->a2 * p->c_pad * p->esize +
@@ -203,12 +215,21 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
       p->splits = (num_kb + kbps - 1) / kbps;
     }
   }
-  p->v_bytes = align_up(static_cast<size_t>(p->nsplit) * p->a2 * p->chunk_tiles * p->c_pad *
-                            p->esize,
-                        1024);
+  p->v_bytes = p->smallc ? 0
+                        : align_up(static_cast<size_t>(p->nsplit) * p->a2 * p->chunk_tiles *
+                                       p->c_pad * p->esize,
+                                   1024);
+  if (p->smallc) {  // no transform-space staging at all
+    p->num_chunks = 1;
+    p->rows_per_chunk = p->rows_total;
+    p->chunk_tiles = p->P;
+    p->splits = 1;
+  }
   p->m_ld = static_cast<long long>(align_up(static_cast<size_t>(p->chunk_tiles), 4));
-  p->m_bytes = align_up(static_cast<size_t>(p->splits) * p->a2 * L.K * p->m_ld * p->acc_bytes,
-                        1024);
+  p->m_bytes = p->smallc ? 0
+                        : align_up(static_cast<size_t>(p->splits) * p->a2 * L.K * p->m_ld *
+                                       p->acc_bytes,
+                                   1024);
   *out = p;
   return WINO_OK;
 }
@@ -243,7 +264,8 @@ int wino_plan_get_info(wino_plan_t p, wino_plan_info_t* info) {
   info->chunk_tiles = p->chunk_tiles;
   info->u_bytes = p->u_bytes;
   info->workspace_bytes = p->u_bytes + p->v_bytes + p->m_bytes;
-  info->launches_per_forward = p->num_chunks * 3;
+  info->launches_per_forward = p->smallc ? 1 : p->num_chunks * 3;
+  info->fused_small_c = p->smallc ? 1 : 0;
   info->multiplies = p->P * p->L.C * static_cast<long long>(p->L.K) * p->a2;
   return WINO_OK;
 }
@@ -312,9 +334,16 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
     U = ws;
     ws += p->u_bytes;
   }
+  const wino_layer_t& L = p->L;
+  if (p->smallc) {
+    cudaError_t e = launch_fused_smallc(p->m, p->prec, d, U, y, L.N, L.C, L.H, L.W, L.K, L.pad,
+                                        p->th, p->tw, p->oh, p->ow, p->c_pad, s);
+    if (e != cudaSuccess) return cuda_fail(e, "fused small-C layer");
+    tm.mark(1);
+    return WINO_OK;
+  }
   void* V = ws;
   void* Mb = ws + p->v_bytes;
-  const wino_layer_t& L = p->L;
   for (int ch = 0; ch < p->num_chunks; ++ch) {
     const int row0 = ch * p->rows_per_chunk;
     const int rows = (row0 + p->rows_per_chunk <= p->rows_total) ? p->rows_per_chunk

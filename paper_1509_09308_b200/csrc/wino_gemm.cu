@@ -105,6 +105,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // prologue above overlaps the predecessor (PDL); operands are read below
+  griddep_launch();
+  griddep_wait();
 
   auto decode = [&](int u, int& pb, int& kbk, int& comp, int& split) {
     pb = u % n_pblk;
@@ -245,6 +248,8 @@ __global__ void __launch_bounds__(256) wgemm_f64_kernel(const double* __restrict
   const double* Vc = V + static_cast<size_t>(comp) * Pc * c_pad;
   const double* Uc = U + static_cast<size_t>(comp) * K * c_pad;
   double acc[4][4] = {};
+  griddep_launch();
+  griddep_wait();
   for (int cb = 0; cb < C; cb += 16) {
     for (int e = threadIdx.x; e < 16 * 64; e += 256) {
       const int r = e / 16, cc = e % 16;
@@ -329,8 +334,8 @@ static cudaError_t launch_tc(const GemmArgs& a, cudaStream_t s) {
   const long long units = static_cast<long long>(n_pblk) * n_kblk * a.a2 * splits;
   if (units > 0x7fffffffLL) return cudaErrorInvalidValue;
   const int grid = static_cast<int>(units < num_sms() ? units : num_sms());
-  kern<<<grid, kGemmThreads, Sm::total, s>>>(tmV, tmU, tmM, a.a2, num_kb, kbps, n_pblk, n_kblk,
-                                             static_cast<int>(units));
+  launch_k(kern, dim3(grid), dim3(kGemmThreads), Sm::total, s, tmV, tmU, tmM, a.a2, num_kb, kbps,
+           n_pblk, n_kblk, static_cast<int>(units));
   return cudaGetLastError();
 }
 
@@ -361,10 +366,9 @@ cudaError_t launch_batched_gemm(int prec, const GemmArgs& a, cudaStream_t s) {
     case kFP16: return launch_prec<kFP16>(a, s);
     case kFP64: {
       const dim3 grid(static_cast<unsigned>((a.Pc + 63) / 64), (a.K + 63) / 64, a.a2);
-      wgemm_f64_kernel<<<grid, 256, 0, s>>>(static_cast<const double*>(a.V),
-                                            static_cast<const double*>(a.U),
-                                            static_cast<double*>(a.M), a.K, a.Pc, a.C, a.c_pad,
-                                            a.m_ld);
+      launch_k(wgemm_f64_kernel, grid, dim3(256), 0, s, static_cast<const double*>(a.V),
+               static_cast<const double*>(a.U), static_cast<double*>(a.M), a.K, a.Pc, a.C,
+               a.c_pad, a.m_ld);
       return cudaGetLastError();
     }
     default: return cudaErrorInvalidValue;

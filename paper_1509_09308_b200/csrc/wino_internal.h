@@ -4,6 +4,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <utility>
+
 #include "../../include/wino.h"
 
 namespace wino {
@@ -45,6 +47,13 @@ cudaError_t launch_output_transform(int m, int prec, const void* Mbuf, void* y, 
                                     int th, int tw, int oh, int ow, int row0, long long Pc,
                                     long long m_ld, int splits, cudaStream_t s);
 
+// Whole layer on chip for C <= 8 (input transform + C-term reduction + output
+// transform in one kernel); U in the plan's operand format.
+constexpr int kSmallCMax = 8;
+cudaError_t launch_fused_smallc(int m, int prec, const void* d, const void* U, void* y, int N,
+                                int C, int H, int W, int K, int pad, int th, int tw, int oh,
+                                int ow, int c_pad, cudaStream_t s);
+
 struct GemmArgs {
   const void* V;   // [nsplit][a2][Pc][c_pad]
   const void* U;   // [nsplit][a2][K][c_pad]
@@ -60,6 +69,36 @@ int gemm_device_sms();
 // Tensor-core (tcgen05) GEMM for FP32/TF32/BF16/FP16, CUDA-core fp64 for FP64.
 cudaError_t launch_batched_gemm(int prec, const GemmArgs& a, cudaStream_t s);
 int gemm_kernels_per_launch(int prec);
+
+// ---- launch helper: every pipeline kernel is launched with Programmatic
+// Dependent Launch allowed (disable with WINO_NO_PDL=1), so its launch and
+// prologue overlap the previous kernel's tail; kernels call griddep_wait()
+// before touching predecessor outputs and griddep_launch() at entry.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+#ifdef __CUDACC__
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+#endif
 
 // Host helpers.
 const char* set_error(const char* fmt, ...);

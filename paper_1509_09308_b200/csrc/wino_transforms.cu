@@ -59,6 +59,9 @@ struct OpStore<kFP64> {
   }
 };
 
+template <int M, typename TA>
+__device__ __forceinline__ void store_tile(TA* dst, int ow, int vr, int vc, const TA (&out)[M][M]);
+
 // ============================================================ filter transform
 // Block = 256 consecutive (k, c) pairs = 256 contiguous 3x3 filters: staged
 // through shared memory with coalesced loads (the 36-byte records would
@@ -73,6 +76,8 @@ __global__ void __launch_bounds__(256) filter_transform_kernel(
   using A = Alg<M>;
   constexpr int AL = A::alpha;
   __shared__ T sg[256 * 9 + 1];
+  griddep_launch();
+  griddep_wait();
   const long long total = static_cast<long long>(K) * C;
   const long long t0 = static_cast<long long>(blockIdx.x) * 256;
   const int nloc = static_cast<int>(min(256LL, total - t0));
@@ -164,6 +169,8 @@ __global__ void __launch_bounds__(256) input_transform_kernel(
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   constexpr int NW = 256 / 32;
+  griddep_launch();
+  griddep_wait();
 
   // ---- phase 1: stage [cb ch][alpha rows][xw] with zero fill.  Every element
   // is an independent cp.async (zero-filled when out of range), so all loads of
@@ -256,6 +263,8 @@ __global__ void __launch_bounds__(128) output_transform_kernel(const TA* __restr
   constexpr int AL = A::alpha;
   const long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int k = blockIdx.y;
+  griddep_launch();
+  griddep_wait();
   if (p >= Pc) return;
   const size_t cstride = static_cast<size_t>(K) * m_ld;
   const size_t sstride = cstride * AL * AL;
@@ -281,11 +290,46 @@ __global__ void __launch_bounds__(128) output_transform_kernel(const TA* __restr
   const int ty = rest / tw, tx = rest - ty * tw;
   const int vr = min(M, oh - M * ty), vc = min(M, ow - M * tx);
   TA* dst = y + ((static_cast<size_t>(n) * K + k) * oh + M * ty) * ow + M * tx;
+  store_tile<M>(dst, ow, vr, vc, out);
+}
+
+// Write an m x m output tile: one vector store per row for full tiles whose
+// rows are vector-aligned (a warp then writes 32 adjacent tiles = whole lines),
+// clipped scalar stores for edge tiles (engine.py:246-253).
+template <int M, typename TA>
+__device__ __forceinline__ void store_tile(TA* dst, int ow, int vr, int vc, const TA (&out)[M][M]) {
+  constexpr int VB = M * sizeof(TA);  // bytes per tile row
+  const bool vec = (vr == M) && (vc == M) && (VB == 8 || VB == 16 || VB == 32) &&
+                   ((reinterpret_cast<uintptr_t>(dst) | (static_cast<size_t>(ow) * sizeof(TA))) %
+                        (VB > 16 ? 16 : VB) ==
+                    0);
+  if (vec) {
 #pragma unroll
-  for (int i = 0; i < M; ++i)
+    for (int i = 0; i < M; ++i) {
+      TA* row = dst + static_cast<size_t>(i) * ow;
+      if constexpr (VB == 8) {
+        if constexpr (sizeof(TA) == 4)
+          *reinterpret_cast<float2*>(row) = make_float2(out[i][0], out[i][1]);
+        else
+          *reinterpret_cast<double*>(row) = out[i][0];
+      } else {
 #pragma unroll
-    for (int j = 0; j < M; ++j)
-      if (i < vr && j < vc) dst[static_cast<size_t>(i) * ow + j] = out[i][j];
+        for (int h = 0; h < VB / 16; ++h) {
+          if constexpr (sizeof(TA) == 4)
+            reinterpret_cast<float4*>(row)[h] =
+                make_float4(out[i][4 * h], out[i][4 * h + 1], out[i][4 * h + 2], out[i][4 * h + 3]);
+          else
+            reinterpret_cast<double2*>(row)[h] = make_double2(out[i][2 * h], out[i][2 * h + 1]);
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < M; ++i)
+#pragma unroll
+      for (int j = 0; j < M; ++j)
+        if (i < vr && j < vc) dst[static_cast<size_t>(i) * ow + j] = out[i][j];
+  }
 }
 
 // ================================================================ launchers
@@ -308,8 +352,8 @@ static void filter_launch(const void* g, void* U, int K, int C, int c_pad, cudaS
     max_carveout(kern);
     configured = true;
   }
-  kern<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(static_cast<const T*>(g), U, K, C,
-                                                              c_pad);
+  launch_k(kern, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s,
+           static_cast<const T*>(g), U, K, C, c_pad);
 }
 
 template <int M>
@@ -349,8 +393,8 @@ static cudaError_t input_one(const void* d, void* V, int N, int C, int H, int W,
     configured = true;
   }
   const dim3 grid((tw + Cfg::tpx - 1) / Cfg::tpx, rows, (C + Cfg::cb - 1) / Cfg::cb);
-  kern<<<grid, 256, smem, s>>>(static_cast<const T*>(d), V, N, C, H, W, pad, th, tw, row0, Pc,
-                               c_pad);
+  launch_k(kern, grid, dim3(256), smem, s, static_cast<const T*>(d), V, N, C, H, W, pad, th, tw,
+           row0, Pc, c_pad);
   return cudaGetLastError();
 }
 
@@ -390,25 +434,186 @@ cudaError_t launch_output_transform(int m, int prec, const void* Mbuf, void* y, 
     configured = true;
   }
   if (prec == kFP64) {
-    if (m == 2)
-      output_transform_kernel<2, double><<<grid, 128, 0, s>>>(
-          static_cast<const double*>(Mbuf), static_cast<double*>(y), N, K, th, tw, oh, ow, row0, Pc,
-          m_ld, splits);
-    else
-      output_transform_kernel<4, double><<<grid, 128, 0, s>>>(
-          static_cast<const double*>(Mbuf), static_cast<double*>(y), N, K, th, tw, oh, ow, row0, Pc,
-          m_ld, splits);
+    launch_k(m == 2 ? output_transform_kernel<2, double> : output_transform_kernel<4, double>, grid,
+             dim3(128), 0, s, static_cast<const double*>(Mbuf), static_cast<double*>(y), N, K, th,
+             tw, oh, ow, row0, Pc, m_ld, splits);
   } else {
-    if (m == 2)
-      output_transform_kernel<2, float><<<grid, 128, 0, s>>>(
-          static_cast<const float*>(Mbuf), static_cast<float*>(y), N, K, th, tw, oh, ow, row0, Pc,
-          m_ld, splits);
-    else
-      output_transform_kernel<4, float><<<grid, 128, 0, s>>>(
-          static_cast<const float*>(Mbuf), static_cast<float*>(y), N, K, th, tw, oh, ow, row0, Pc,
-          m_ld, splits);
+    launch_k(m == 2 ? output_transform_kernel<2, float> : output_transform_kernel<4, float>, grid,
+             dim3(128), 0, s, static_cast<const float*>(Mbuf), static_cast<float*>(y), N, K, th,
+             tw, oh, ow, row0, Pc, m_ld, splits);
   }
   return cudaGetLastError();
+}
+
+// ====================================================== fused tiny-C layer
+// For C <= 8 (VGG conv1.1 has C = 3) the alpha^2 GEMMs reduce over only C
+// terms, so the transform-space intermediates (alpha^2*C*P + alpha^2*K*P
+// values) dwarf the layer's input.  This kernel runs the whole layer on chip:
+// block = 32 consecutive tiles of one tile row x all K filters.
+//   1. stage the C x alpha x (32m+2) input window in smem (zero padding)
+//   2. warp c forms V[comp][c][t] = B^T d B for the 32 tiles (smem)
+//   3. filters in chunks of 32: U chunk -> smem (fp32, from the operand-format
+//      stack), thread (tile = lane, filter) forms M[comp] = sum_c U V,
+//      Y = A^T M A, and stores the m x m tile (vector rows).
+// Arithmetic is fp32 (fp64 for FP64): at least the precision of the
+// tensor-core path it replaces.
+constexpr int kSmallC = 8;
+constexpr int kSmallKB = 32;
+
+template <int PREC>
+__device__ __forceinline__ float load_op(const void* U, size_t idx, size_t plane) {
+  if constexpr (PREC == kFP32) {
+    const float* u = static_cast<const float*>(U);
+    return u[idx] + u[idx + plane];  // hi + lo = the exact fp32 transform
+  } else if constexpr (PREC == kTF32) {
+    return static_cast<const float*>(U)[idx];
+  } else if constexpr (PREC == kBF16) {
+    return __bfloat162float(static_cast<const __nv_bfloat16*>(U)[idx]);
+  } else {
+    return __half2float(static_cast<const __half*>(U)[idx]);
+  }
+}
+
+template <int M, int PREC, int CP>
+__global__ void __launch_bounds__(256) fused_smallc_kernel(
+    const typename OpStore<PREC>::T* __restrict__ d, const void* __restrict__ U,
+    typename OpStore<PREC>::T* __restrict__ y, int C, int H, int W, int K, int pad, int th,
+    int tw, int oh, int ow, int c_pad) {
+  using T = typename OpStore<PREC>::T;
+  using A = Alg<M>;
+  constexpr int AL = A::alpha;
+  constexpr int A2 = AL * AL;
+  constexpr int XW = 32 * M + 2;
+  // CP = C padded to {2,4,8}: channel loops are compile-time, padded channels
+  // are zero in both the staged input and the staged filters.
+  // smem: in[CP][AL][XW] | v[A2][CP][32] | u[A2][KB][CP]
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* s_u = reinterpret_cast<T*>(smem_raw);  // first: 16-byte aligned rows of CP values
+  T* s_v = s_u + A2 * kSmallKB * CP;
+  T* s_in = s_v + A2 * CP * 32;
+
+  const int row = blockIdx.y;  // n*th + ty
+  const int n = row / th, ty = row - (row / th) * th;
+  const int tx0 = blockIdx.x * 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int y0 = M * ty - pad, x0 = M * tx0 - pad;
+  griddep_launch();
+  griddep_wait();
+
+  for (int r = warp; r < CP * AL; r += 8) {  // row (c, i): lanes along x
+    const int c = r / AL, i = r - (r / AL) * AL;
+    const int gy = y0 + i;
+    const bool rowok = c < C && gy >= 0 && gy < H;
+    const T* src = d + (rowok ? ((static_cast<size_t>(n) * C + c) * H + gy) * W : 0);
+    for (int x = lane; x < XW; x += 32) {
+      const int gx = x0 + x;
+      s_in[r * XW + x] = (rowok && gx >= 0 && gx < W) ? __ldg(src + gx) : T(0);
+    }
+  }
+  __syncthreads();
+  for (int c = warp; c < CP; c += 8) {
+    T in[AL][AL], out[AL][AL];
+#pragma unroll
+    for (int i = 0; i < AL; ++i)
+#pragma unroll
+      for (int j = 0; j < AL; ++j) in[i][j] = s_in[(c * AL + i) * XW + lane * M + j];
+    sandwich<T, AL, AL>(in, out, [](int i, int j) { return A::BT(i, j); });
+#pragma unroll
+    for (int xi = 0; xi < AL; ++xi)
+#pragma unroll
+      for (int nu = 0; nu < AL; ++nu) s_v[((xi * AL + nu) * CP + c) * 32 + lane] = out[xi][nu];
+  }
+  const int t = tx0 + lane;
+  const size_t plane = static_cast<size_t>(A2) * K * c_pad;
+  for (int kc = 0; kc < K; kc += kSmallKB) {
+    const int kn = min(kSmallKB, K - kc);
+    __syncthreads();  // s_v ready / previous s_u chunk consumed
+    for (int e = threadIdx.x; e < A2 * kSmallKB * CP; e += 256) {
+      const int c = e % CP, r = e / CP;
+      const int kk = r % kSmallKB, comp = r / kSmallKB;
+      T v = T(0);
+      if (c < C && kk < kn) {
+        const size_t idx = (static_cast<size_t>(comp) * K + kc + kk) * c_pad + c;
+        if constexpr (PREC == kFP64)
+          v = static_cast<const double*>(U)[idx];
+        else
+          v = load_op<PREC>(U, idx, plane);
+      }
+      s_u[e] = v;
+    }
+    __syncthreads();
+    if (t >= tw) continue;
+    for (int kk = warp; kk < kn; kk += 8) {
+      T mm[AL][AL];
+      const T* urow = s_u + kk * CP;
+#pragma unroll
+      for (int comp = 0; comp < A2; ++comp) {
+        const T* uc = urow + comp * kSmallKB * CP;
+        const T* vc = s_v + comp * CP * 32 + lane;
+        T acc = uc[0] * vc[0];
+#pragma unroll
+        for (int c = 1; c < CP; ++c) acc = fma(uc[c], vc[c * 32], acc);
+        mm[comp / AL][comp % AL] = acc;
+      }
+      T out[M][M];
+      sandwich<T, M, AL>(mm, out, [](int i, int j) { return A::AT(i, j); });
+      const int k = kc + kk;
+      const int vr = min(M, oh - M * ty), vc = min(M, ow - M * t);
+      T* dst = y + ((static_cast<size_t>(n) * K + k) * oh + M * ty) * ow + M * t;
+      store_tile<M>(dst, ow, vr, vc, out);
+    }
+  }
+}
+
+template <int M, int PREC, int CP>
+static cudaError_t smallc_one(const void* d, const void* U, void* y, int N, int C, int H, int W,
+                              int K, int pad, int th, int tw, int oh, int ow, int c_pad,
+                              cudaStream_t s) {
+  using T = typename OpStore<PREC>::T;
+  auto kern = fused_smallc_kernel<M, PREC, CP>;
+  constexpr int AL = M + 2, A2 = AL * AL, XW = 32 * M + 2;
+  constexpr size_t smem = sizeof(T) * (A2 * kSmallKB * CP + A2 * CP * 32 + CP * AL * XW);
+  static bool configured = false;
+  if (!configured) {
+    max_carveout(kern);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    configured = true;
+  }
+  const dim3 grid((tw + 31) / 32, N * th);
+  launch_k(kern, grid, dim3(256), smem, s, static_cast<const T*>(d), U, static_cast<T*>(y), C, H,
+           W, K, pad, th, tw, oh, ow, c_pad);
+  return cudaGetLastError();
+}
+
+template <int M, int PREC>
+static cudaError_t smallc_cp(const void* d, const void* U, void* y, int N, int C, int H, int W,
+                             int K, int pad, int th, int tw, int oh, int ow, int c_pad,
+                             cudaStream_t s) {
+  if (C <= 2) return smallc_one<M, PREC, 2>(d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
+  if (C <= 4) return smallc_one<M, PREC, 4>(d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
+  return smallc_one<M, PREC, 8>(d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
+}
+
+template <int M>
+static cudaError_t smallc_dispatch(int prec, const void* d, const void* U, void* y, int N, int C,
+                                   int H, int W, int K, int pad, int th, int tw, int oh, int ow,
+                                   int c_pad, cudaStream_t s) {
+  switch (prec) {
+    case kFP32: return smallc_cp<M, kFP32>(d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
+    case kTF32: return smallc_cp<M, kTF32>(d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
+    case kBF16: return smallc_cp<M, kBF16>(d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
+    case kFP16: return smallc_cp<M, kFP16>(d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
+    case kFP64: return smallc_cp<M, kFP64>(d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_fused_smallc(int m, int prec, const void* d, const void* U, void* y, int N,
+                                int C, int H, int W, int K, int pad, int th, int tw, int oh,
+                                int ow, int c_pad, cudaStream_t s) {
+  if (C > kSmallC) return cudaErrorInvalidValue;
+  return m == 2 ? smallc_dispatch<2>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s)
+                : smallc_dispatch<4>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
 }
 
 }  // namespace wino
