@@ -95,6 +95,29 @@ bool pdl_enabled() {
   return on;
 }
 
+bool encode_tmap_nchw_f32(void* map_out, const void* base, int N, int C, int H, int W,
+                          uint32_t box_w, uint32_t box_h, uint32_t box_c) {
+  if (!load_encode()) {
+    set_error("cuTensorMapEncodeTiled unavailable (driver too old?)");
+    return false;
+  }
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
+                        static_cast<cuuint64_t>(C), static_cast<cuuint64_t>(N)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(W) * 4, static_cast<cuuint64_t>(H) * W * 4,
+                           static_cast<cuuint64_t>(C) * H * W * 4};
+  cuuint32_t box[4] = {box_w, box_h, box_c, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = g_encode(reinterpret_cast<CUtensorMap*>(map_out), CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                        4, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (NCHW) failed (%d)", (int)r);
+    return false;
+  }
+  return true;
+}
+
 static int cuda_fail(cudaError_t e, const char* what) {
   if (e == cudaErrorMemoryAllocation) {
     set_error("%s: out of device memory", what);

@@ -102,6 +102,9 @@ __device__ __forceinline__ void griddep_launch() {
 
 // Host helpers.
 const char* set_error(const char* fmt, ...);
+// 4D fp32 map over an NCHW tensor (dims W,H,C,N), no swizzle, zero OOB fill.
+bool encode_tmap_nchw_f32(void* map_out, const void* base, int N, int C, int H, int W,
+                          uint32_t box_w, uint32_t box_h, uint32_t box_c);
 bool encode_tmap_3d(void* map_out, int prec, const void* base, uint64_t d0, uint64_t d1,
                     uint64_t d2, uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box0,
                     uint32_t box1);

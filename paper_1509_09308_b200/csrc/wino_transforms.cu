@@ -5,6 +5,9 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <cstdlib>
+
+#include "sm100_ptx.cuh"
 #include "wino_internal.h"
 #include "winograd_mats.cuh"
 
@@ -156,7 +159,7 @@ __global__ void __launch_bounds__(256) input_transform_kernel(
   using Cfg = InCfg<M, PREC>;
   constexpr int AL = A::alpha;
   constexpr int CPL = Cfg::cpl;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   T* s = reinterpret_cast<T*>(smem_raw);
 
   const int row = row0 + blockIdx.y;  // global tile row = n*th + ty
@@ -377,11 +380,148 @@ cudaError_t launch_filter_transform(int m, int prec, const void* g, void* U, int
                 : filter_dispatch<4>(prec, g, U, K, C, c_pad, s);
 }
 
+// ------------------------------------------------ TMA-staged input transform
+// Fast path for fp32 data with 16-byte-aligned rows (W % 4 == 0): one 4D TMA
+// box (x, y, channel) per block stages the window, zero-filling the padding
+// and channels >= C in hardware (negative start coordinates are legal).
+// The box's innermost start coordinate must be 16-byte aligned (otherwise the
+// load faults -- tools/probes/tma_grid_probe.cu), so the box starts SH = (-pad)
+// mod 4 columns left of the window.  It carries alpha+1 rows and XWB = 4*odd
+// columns so each channel plane is an odd number of 16-byte units: lane =
+// channel then reads its patch rows with conflict-free LDS.128.
+// Block = 32 channels x 16 tiles; warp w transforms tiles w and w+8.
+template <int M, int SH>
+struct InTma {
+  static constexpr int alpha = M + 2;
+  static constexpr int tpx = 16;
+  static constexpr int rows = alpha + 1;
+  static constexpr int xwb = (M == 2) ? 44 : 76;  // >= SH + 16*M + 2, 4*odd
+  static constexpr int plane = rows * xwb;
+  static constexpr int bytes = 32 * plane * 4;
+  static constexpr int nv = (M == 2) ? 2 : 3;     // float4 reads per patch row
+  static_assert((plane / 4) % 2 == 1, "plane must be an odd number of 16-byte units");
+  static_assert(SH + tpx * M + 2 <= xwb, "box too narrow");
+};
+
+template <int M, int AL, int NV, int OFF>
+__device__ __forceinline__ void load_patch(const float* sc, int xwb, int base, float (&in)[AL][AL]) {
+#pragma unroll
+  for (int i = 0; i < AL; ++i) {
+    float r[4 * NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const float4 q = *reinterpret_cast<const float4*>(sc + i * xwb + base + 4 * v);
+      r[4 * v] = q.x;
+      r[4 * v + 1] = q.y;
+      r[4 * v + 2] = q.z;
+      r[4 * v + 3] = q.w;
+    }
+#pragma unroll
+    for (int j = 0; j < AL; ++j) in[i][j] = r[OFF + j];
+  }
+}
+
+template <int M, int PREC, int SH>
+__global__ void __launch_bounds__(256) input_transform_tma_kernel(
+    const __grid_constant__ CUtensorMap tmD, void* __restrict__ V, int C, int pad, int th,
+    int tw, int row0, long long Pc, int c_pad) {
+  using A = Alg<M>;
+  using Cfg = InTma<M, SH>;
+  constexpr int AL = A::alpha;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* s = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                      ~static_cast<uintptr_t>(1023));
+  __shared__ uint64_t bar;
+
+  const int row = row0 + blockIdx.y;
+  const int n = row / th;
+  const int ty = row - n * th;
+  const int tx0 = blockIdx.x * Cfg::tpx;
+  const int c0 = blockIdx.z * 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  griddep_launch();
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bar, 1);
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  griddep_wait();
+  if (threadIdx.x == 0) {
+    ptx::mbar_arrive_expect_tx(&bar, Cfg::bytes);
+    ptx::tma_load_4d(s, &tmD, &bar, M * tx0 - pad - SH, M * ty - pad, c0, n);
+  }
+  ptx::mbar_wait(&bar, 0);
+
+  const int c = c0 + lane;
+  if (c >= C) return;
+  const size_t plane_v = static_cast<size_t>(AL) * AL * Pc * c_pad;
+  const size_t comp_stride = static_cast<size_t>(Pc) * c_pad;
+  const float* sc = s + lane * Cfg::plane;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int t = warp + 8 * h;
+    if (tx0 + t >= tw) break;
+    float in[AL][AL];
+    const int x = SH + t * M;  // window column of the patch
+    if constexpr (M == 4) {
+      load_patch<M, AL, Cfg::nv, SH>(sc, Cfg::xwb, x - SH, in);
+    } else {  // F(2x2): the in-float4 offset depends on the (warp-uniform) tile parity
+      constexpr int O0 = SH & 3, O1 = (SH + 2) & 3;
+      if (t & 1)
+        load_patch<M, AL, Cfg::nv, O1>(sc, Cfg::xwb, x - O1, in);
+      else
+        load_patch<M, AL, Cfg::nv, O0>(sc, Cfg::xwb, x - O0, in);
+    }
+    float out[AL][AL];
+    sandwich<float, AL, AL>(in, out, [](int i, int j) { return A::BT(i, j); });
+    const long long p = static_cast<long long>(blockIdx.y) * tw + tx0 + t;
+    size_t idx = static_cast<size_t>(p) * c_pad + c;
+#pragma unroll
+    for (int xi = 0; xi < AL; ++xi)
+#pragma unroll
+      for (int nu = 0; nu < AL; ++nu) {
+        OpStore<PREC>::put(V, idx, plane_v, out[xi][nu]);
+        idx += comp_stride;
+      }
+  }
+}
+
+template <int M, int PREC, int SH>
+static cudaError_t input_tma_launch(const void* d, void* V, int N, int C, int H, int W, int pad,
+                                    int th, int tw, int row0, int rows, long long Pc, int c_pad,
+                                    cudaStream_t s) {
+  using Cfg = InTma<M, SH>;
+  alignas(64) CUtensorMap tmD;
+  if (!encode_tmap_nchw_f32(&tmD, d, N, C, H, W, Cfg::xwb, Cfg::rows, 32))
+    return cudaErrorInvalidValue;
+  auto kern = input_transform_tma_kernel<M, PREC, SH>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::bytes + 1024);
+    max_carveout(kern);
+    configured = true;
+  }
+  const dim3 grid((tw + Cfg::tpx - 1) / Cfg::tpx, rows, (C + 31) / 32);
+  launch_k(kern, grid, dim3(256), static_cast<size_t>(Cfg::bytes + 1024), s, tmD, V, C, pad, th,
+           tw, row0, Pc, c_pad);
+  return cudaGetLastError();
+}
+
 template <int M, int PREC>
 static cudaError_t input_one(const void* d, void* V, int N, int C, int H, int W, int pad, int th,
                              int tw, int row0, int rows, long long Pc, int c_pad,
                              cudaStream_t s) {
   using T = typename OpStore<PREC>::T;
+  if constexpr (PREC != kFP64) {
+    if (W % 4 == 0 && pad <= 3 && getenv("WINO_NO_TMA_INPUT") == nullptr) {
+      switch ((4 - pad % 4) % 4) {  // box shift that makes the start column 16-byte aligned
+        case 0: return input_tma_launch<M, PREC, 0>(d, V, N, C, H, W, pad, th, tw, row0, rows, Pc, c_pad, s);
+        case 1: return input_tma_launch<M, PREC, 1>(d, V, N, C, H, W, pad, th, tw, row0, rows, Pc, c_pad, s);
+        case 2: return input_tma_launch<M, PREC, 2>(d, V, N, C, H, W, pad, th, tw, row0, rows, Pc, c_pad, s);
+        default: return input_tma_launch<M, PREC, 3>(d, V, N, C, H, W, pad, th, tw, row0, rows, Pc, c_pad, s);
+      }
+    }
+  }
   using Cfg = InCfg<M, PREC>;
   const size_t smem = sizeof(T) * Cfg::cb * Cfg::plane;
   auto kern = input_transform_kernel<M, PREC>;
@@ -487,7 +627,7 @@ __global__ void __launch_bounds__(256) fused_smallc_kernel(
   // CP = C padded to {2,4,8}: channel loops are compile-time, padded channels
   // are zero in both the staged input and the staged filters.
   // smem: in[CP][AL][XW] | v[A2][CP][32] | u[A2][KB][CP]
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   T* s_u = reinterpret_cast<T*>(smem_raw);  // first: 16-byte aligned rows of CP values
   T* s_v = s_u + A2 * kSmallKB * CP;
   T* s_in = s_v + A2 * CP * 32;
