@@ -256,8 +256,10 @@ __global__ void __launch_bounds__(256) input_transform_kernel(
 // M[s][comp][k][p] (coalesced over p; split-C slices summed in ascending s),
 // forms A^T M A and writes the valid vr x vc corner of the m x m tile (edge
 // tiles clipped, engine.py:241-254).
+// 128 threads x >= 8 blocks/SM: a latency-bound stream needs the occupancy
+// (unbounded, ptxas spends 168 registers on 36 live addresses).
 template <int M, typename TA>
-__global__ void __launch_bounds__(128) output_transform_kernel(const TA* __restrict__ Mbuf,
+__global__ void __launch_bounds__(128, 8) output_transform_kernel(const TA* __restrict__ Mbuf,
                                                                TA* __restrict__ y, int N, int K,
                                                                int th, int tw, int oh, int ow,
                                                                int row0, long long Pc,
