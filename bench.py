@@ -46,6 +46,25 @@ def gflop_direct(N, C, H, K):
     return 2.0 * N * C * K * H * H * 9 / 1e9  # pad 1: out = H
 
 
+def load_traffic(algo, prec, batch, stage):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu launch
+    list for this workload (profiles/*/traffic.json), or None."""
+    import glob
+    kern = {"batched_gemm": "wgemm_tc_kernel", "input_transform": "input_transform_tma_kernel",
+            "output_transform": "output_transform_kernel",
+            "filter_transform": "filter_transform_kernel"}[stage]
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "traffic.json")), reverse=True):
+        try:
+            with open(path) as fh:
+                tab = json.load(fh)
+            hit = tab.get(f"{algo}:{prec}:N{batch}", {}).get(kern)
+            if hit is not None:
+                return hit
+        except Exception:
+            pass
+    return None
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -56,45 +75,49 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+    """nvidia-smi clocks + throttle reasons sampled (every 20 ms) while the
+    timed region runs; one long-lived `nvidia-smi -lms` process."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
         self.samples = []
-        self._stop = threading.Event()
-        self._t = threading.Thread(target=self._run, daemon=True)
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.1)
+        self._p = None
 
     def __enter__(self):
-        self._t.start()
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                        "--format=csv,noheader,nounits", "-lms", "20"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)  # let the sampler start before the timed region
+        except Exception:
+            self._p = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self._p is None:
+            return
+        time.sleep(0.05)
+        self._p.terminate()
+        try:
+            out, _ = self._p.communicate(timeout=5)
+        except Exception:
+            self._p.kill()
+            out = ""
+        for line in out.strip().splitlines():
+            self.samples.append([x.strip() for x in line.split(",")])
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        num = lambda x: x.replace(".", "", 1).isdigit()
+        sm = [float(s[0]) for s in self.samples if num(s[0])]
+        mx = [float(s[1]) for s in self.samples if len(s) > 1 and num(s[1])]
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
         reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
                 "samples": len(self.samples)}
@@ -367,6 +390,10 @@ def run_gpu(args) -> None:
         achieved = stage_bytes[dom] / max(stage_n[dom], 1) / (avg_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": None}
+    traffic = load_traffic(args.algo, prec, B, STAGES[dom])
+    if traffic is not None:
+        roof["traffic"] = traffic
+        roof["traffic_source"] = "ncu dram__bytes_read.sum+write.sum per launch (profiles/)"
     roof.update({"kernel": STAGES[dom], "peak_source": f"{peak_src} (MEASURED_PEAKS.json)"
                  if peak_src == "measured" else "fallback (B200_PROFILING.md)",
                  "avg_launch_ms": avg_ms, "launches": stage_n[dom],
@@ -441,7 +468,7 @@ def run_gpu(args) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--algo", default="f2x2")
