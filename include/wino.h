@@ -71,6 +71,8 @@ typedef struct {
   int launches_per_forward;   /* kernels launched by one wino_forward (U given)  */
   int fused_small_c;          /* 1: C <= 8, whole layer in one fused kernel      */
   long long multiplies;       /* P*C*K*alpha^2: the reference "mul" counter      */
+  int fused;                  /* 1: fused Winograd-GEMM kernel (no V/M staging)  */
+  int fused_splits;           /* split-C factor of the fused kernel              */
 } wino_plan_info_t;
 
 /* Create a plan.  m in {2,4} (F(2x2,3x3), F(4x4,3x3)); R == S == 3.

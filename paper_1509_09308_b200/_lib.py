@@ -47,6 +47,7 @@ class PlanInfo(ctypes.Structure):
         ("u_bytes", ctypes.c_size_t), ("workspace_bytes", ctypes.c_size_t),
         ("launches_per_forward", ctypes.c_int), ("fused_small_c", ctypes.c_int),
         ("multiplies", ctypes.c_longlong),
+        ("fused", ctypes.c_int), ("fused_splits", ctypes.c_int),
     ]
 
     def as_dict(self) -> dict:

@@ -1,16 +1,22 @@
-"""In-tree build of libwino.so for sm_100a (nvcc; no JIT cache, no pip install)."""
+"""In-tree build of libwino.so for sm_100a (nvcc; no JIT cache, no pip install).
+
+Each translation unit compiles to its own object in parallel (the tcgen05
+kernels are template-heavy), then one nvcc link produces the shared object.
+"""
 from __future__ import annotations
 
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(HERE, "_obj")
 OUT = os.path.join(HERE, "libwino.so")
-SOURCES = ("wino_api.cu", "wino_transforms.cu", "wino_gemm.cu")
-NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3",
-              "-std=c++17", "-Xcompiler", "-fPIC", "-shared"]
+SOURCES = ("wino_api.cu", "wino_transforms.cu", "wino_gemm.cu", "wino_fused.cu")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = [*ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC"]
 
 
 def _nvcc() -> str:
@@ -18,6 +24,24 @@ def _nvcc() -> str:
         if cand and (os.path.isabs(cand) and os.path.exists(cand) or not os.path.isabs(cand)):
             return cand
     return "nvcc"
+
+
+def _headers():
+    hs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
+    hs.append(os.path.join(HERE, "..", "include", "wino.h"))
+    return [h for h in hs if os.path.exists(h)]
+
+
+def _obj(src: str) -> str:
+    return os.path.join(OBJ, os.path.splitext(src)[0] + ".o")
+
+
+def _stale(src: str, hdr_time: float) -> bool:
+    o = _obj(src)
+    if not os.path.exists(o):
+        return True
+    t = os.path.getmtime(o)
+    return os.path.getmtime(os.path.join(CSRC, src)) > t or hdr_time > t
 
 
 def needs_build() -> bool:
@@ -32,8 +56,19 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return OUT
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", OUT + ".tmp",
-           *[os.path.join(CSRC, s) for s in SOURCES]]
+    os.makedirs(OBJ, exist_ok=True)
+    hdr_time = max(os.path.getmtime(h) for h in _headers())
+    todo = [s for s in SOURCES if force or _stale(s, hdr_time)]
+
+    def compile_one(src: str) -> None:
+        cmd = [_nvcc(), *NVCC_FLAGS, "-c", "-o", _obj(src), os.path.join(CSRC, src)]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(todo), os.cpu_count() or 1))) as ex:
+        list(ex.map(compile_one, todo))
+    cmd = [_nvcc(), *ARCH, "-shared", "-o", OUT + ".tmp", *[_obj(s) for s in SOURCES]]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

@@ -23,6 +23,9 @@ struct wino_plan_s {
   int c_pad, esize, nsplit, acc_bytes;
   int bn, splits;
   bool smallc;  // whole layer in the fused tiny-C kernel (no V/M staging)
+  bool fused;   // fused Winograd-GEMM (transforms inside the tcgen05 kernel)
+  int fsplits;  // split-C factor of the fused kernel
+  size_t ypart_bytes;
   int rows_total, rows_per_chunk, num_chunks;
   long long chunk_tiles;
   long long m_ld;                    // M row stride (tiles, multiple of 4)
@@ -82,6 +85,34 @@ bool encode_tmap_3d(void* map_out, int prec, const void* base, uint64_t d0, uint
     set_error("cuTensorMapEncodeTiled failed (%d): dims %llu,%llu,%llu strides %llu,%llu", (int)r,
               (unsigned long long)d0, (unsigned long long)d1, (unsigned long long)d2,
               (unsigned long long)stride1_bytes, (unsigned long long)stride2_bytes);
+    return false;
+  }
+  return true;
+}
+
+// Operand map with an explicit swizzle span (32 / 64 / 128 bytes per box row).
+bool encode_tmap_3d_sw(void* map_out, int prec, const void* base, uint64_t d0, uint64_t d1,
+                       uint64_t d2, uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box0,
+                       uint32_t box1, int swizzle_bytes) {
+  if (!load_encode()) {
+    set_error("cuTensorMapEncodeTiled unavailable (driver too old?)");
+    return false;
+  }
+  CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  if (prec == kBF16) dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  if (prec == kFP16) dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  const CUtensorMapSwizzle sw = swizzle_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                      : CU_TENSOR_MAP_SWIZZLE_32B;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
+  cuuint32_t box[3] = {box0, box1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(reinterpret_cast<CUtensorMap*>(map_out), dt, 3, const_cast<void*>(base),
+                        dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (swizzle %d) failed (%d)", swizzle_bytes, (int)r);
     return false;
   }
   return true;
@@ -249,7 +280,35 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
     p->splits = 1;
   }
   p->m_ld = static_cast<long long>(align_up(static_cast<size_t>(p->chunk_tiles), 4));
-  p->m_bytes = p->smallc ? 0
+  // ---- path: fused Winograd-GEMM (default) or the staged pipeline.
+  // WINO_PATH=fused|unfused|auto overrides (read at plan creation).
+  {
+    const char* env = getenv("WINO_PATH");
+    const bool force_unfused = env && strcmp(env, "unfused") == 0;
+    p->fused = !p->smallc && prec != kFP64 && !force_unfused;
+  }
+  p->fsplits = 1;
+  p->ypart_bytes = 0;
+  if (p->fused) {
+    const int sms = gemm_device_sms();
+    const int num_kb = fused_num_kblocks(prec, L.C);
+    const int pbt = fused_tiles_per_unit(m);
+    const long long ctas = ((p->P + pbt - 1) / pbt) * ((L.K + 127) / 128) * p->alpha;
+    if (ctas < sms && num_kb > 1) {
+      int sp = static_cast<int>((sms + ctas - 1) / ctas);
+      if (sp > num_kb) sp = num_kb;
+      const int kbps = (num_kb + sp - 1) / sp;
+      p->fsplits = (num_kb + kbps - 1) / kbps;
+    }
+    if (p->fsplits > 1)
+      p->ypart_bytes = align_up(static_cast<size_t>(p->fsplits) * L.N * L.K * oh * ow * 4, 1024);
+    p->num_chunks = 1;
+    p->rows_per_chunk = p->rows_total;
+    p->chunk_tiles = p->P;
+    p->splits = 1;
+    p->v_bytes = 0;
+  }
+  p->m_bytes = (p->smallc || p->fused) ? 0
                         : align_up(static_cast<size_t>(p->splits) * p->a2 * L.K * p->m_ld *
                                        p->acc_bytes,
                                    1024);
@@ -286,8 +345,11 @@ int wino_plan_get_info(wino_plan_t p, wino_plan_info_t* info) {
   info->num_chunks = p->num_chunks;
   info->chunk_tiles = p->chunk_tiles;
   info->u_bytes = p->u_bytes;
-  info->workspace_bytes = p->u_bytes + p->v_bytes + p->m_bytes;
-  info->launches_per_forward = p->smallc ? 1 : p->num_chunks * 3;
+  info->workspace_bytes = p->u_bytes + p->v_bytes + p->m_bytes + p->ypart_bytes;
+  info->launches_per_forward =
+      p->smallc ? 1 : (p->fused ? (p->fsplits > 1 ? 2 : 1) : p->num_chunks * 3);
+  info->fused = p->fused ? 1 : 0;
+  info->fused_splits = p->fsplits;
   info->fused_small_c = p->smallc ? 1 : 0;
   info->multiplies = p->P * p->L.C * static_cast<long long>(p->L.K) * p->a2;
   return WINO_OK;
@@ -345,7 +407,7 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   StageTimer tm(s, timer);
   unsigned char* ws = static_cast<unsigned char*>(workspace);
-  size_t need = p->v_bytes + p->m_bytes + (U ? 0 : p->u_bytes);
+  size_t need = p->v_bytes + p->m_bytes + p->ypart_bytes + (U ? 0 : p->u_bytes);
   if (workspace_bytes < need) {
     set_error("workspace too small: %zu < %zu bytes", workspace_bytes, need);
     return WINO_EINVAL;
@@ -363,6 +425,17 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
                                         p->th, p->tw, p->oh, p->ow, p->c_pad, s);
     if (e != cudaSuccess) return cuda_fail(e, "fused small-C layer");
     tm.mark(1);
+    return WINO_OK;
+  }
+  if (p->fused) {
+    FusedArgs fa{d, U, y, ws, p->P, L.N, L.C, L.H, L.W, L.K, L.pad, p->th, p->tw, p->oh, p->ow,
+                 p->c_pad, p->fsplits};
+    cudaError_t e = launch_fused(p->m, p->prec, fa, s);
+    if (e != cudaSuccess) {
+      if (g_err.empty()) return cuda_fail(e, "fused winograd gemm");
+      return WINO_ECUDA;
+    }
+    tm.mark(2);
     return WINO_OK;
   }
   void* V = ws;

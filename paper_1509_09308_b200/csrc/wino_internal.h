@@ -70,6 +70,23 @@ int gemm_device_sms();
 cudaError_t launch_batched_gemm(int prec, const GemmArgs& a, cudaStream_t s);
 int gemm_kernels_per_launch(int prec);
 
+// Fused Winograd-GEMM (wino_fused.cu): input transform in the producer warps,
+// tcgen05 GEMM, output transform in the epilogue; one cluster of alpha CTAs per
+// (tile block, filter block).  splits > 1 writes partial y slices to ypart
+// ([splits][N][K][oh][ow] fp32) and sums them in a second kernel.
+struct FusedArgs {
+  const void* d;  // (N,C,H,W) fp32
+  const void* U;  // [nsplit][a2][K][c_pad] operand format
+  void* y;        // (N,K,oh,ow) fp32
+  void* ypart;    // split partials (splits > 1)
+  long long P;
+  int N, C, H, W, K, pad, th, tw, oh, ow, c_pad;
+  int splits;
+};
+int fused_num_kblocks(int prec, int C);
+int fused_tiles_per_unit(int m);
+cudaError_t launch_fused(int m, int prec, const FusedArgs& f, cudaStream_t s);
+
 // ---- launch helper: every pipeline kernel is launched with Programmatic
 // Dependent Launch allowed (disable with WINO_NO_PDL=1), so its launch and
 // prologue overlap the previous kernel's tail; kernels call griddep_wait()
@@ -105,6 +122,9 @@ const char* set_error(const char* fmt, ...);
 // 4D fp32 map over an NCHW tensor (dims W,H,C,N), no swizzle, zero OOB fill.
 bool encode_tmap_nchw_f32(void* map_out, const void* base, int N, int C, int H, int W,
                           uint32_t box_w, uint32_t box_h, uint32_t box_c);
+bool encode_tmap_3d_sw(void* map_out, int prec, const void* base, uint64_t d0, uint64_t d1,
+                       uint64_t d2, uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box0,
+                       uint32_t box1, int swizzle_bytes);
 bool encode_tmap_3d(void* map_out, int prec, const void* base, uint64_t d0, uint64_t d1,
                     uint64_t d2, uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box0,
                     uint32_t box1);
