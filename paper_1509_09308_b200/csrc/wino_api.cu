@@ -23,7 +23,7 @@ struct wino_plan_s {
   int c_pad, esize, nsplit, acc_bytes;
   int bn, splits;
   bool smallc;  // whole layer in the fused tiny-C kernel (no V/M staging)
-  bool fused;   // fused Winograd-GEMM (transforms inside the tcgen05 kernel)
+  int path;     // kPathStaged / kPathFused / kPathHybrid (see plan_create)
   int fsplits;  // split-C factor of the fused kernel
   size_t ypart_bytes;
   int rows_total, rows_per_chunk, num_chunks;
@@ -33,6 +33,8 @@ struct wino_plan_s {
 };
 
 namespace wino {
+
+enum : int { kPathStaged = 0, kPathFused = 1, kPathHybrid = 2 };
 
 static thread_local std::string g_err;
 
@@ -280,35 +282,63 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
     p->splits = 1;
   }
   p->m_ld = static_cast<long long>(align_up(static_cast<size_t>(p->chunk_tiles), 4));
-  // ---- path: fused Winograd-GEMM (default) or the staged pipeline.
-  // WINO_PATH=fused|unfused|auto overrides (read at plan creation).
-  {
+  // ---- path (WINO_PATH=staged|fused|hybrid overrides the choice; read at
+  // plan creation):
+  //   staged : input transform -> GEMM -> output transform, V and M staged;
+  //   fused  : one kernel, V formed in the GEMM producer, inverse transform in
+  //            the epilogue (no V, no M);
+  //   hybrid : staged input transform into an L2-sized V chunk, then the fused
+  //            GEMM + inverse-transform kernel TMA-loads it (no M).
+  // Default: staged -- on B200 it measured fastest on every VGG-E layer at
+  // N = 1 and 64 (the alpha-way component split of the fused
+  // kernels cuts TMEM tile reuse alpha-fold and adds an L2/DSMEM exchange).
+  p->path = kPathStaged;
+  if (!p->smallc && prec != kFP64) {
     const char* env = getenv("WINO_PATH");
-    const bool force_unfused = env && strcmp(env, "unfused") == 0;
-    p->fused = !p->smallc && prec != kFP64 && !force_unfused;
+    if (env && (strcmp(env, "staged") == 0 || strcmp(env, "unfused") == 0)) p->path = kPathStaged;
+    if (env && strcmp(env, "fused") == 0) p->path = kPathFused;
+    if (env && strcmp(env, "hybrid") == 0) p->path = kPathHybrid;
   }
   p->fsplits = 1;
   p->ypart_bytes = 0;
-  if (p->fused) {
-    const int sms = gemm_device_sms();
-    const int num_kb = fused_num_kblocks(prec, L.C);
-    const int pbt = fused_tiles_per_unit(m);
-    const long long ctas = ((p->P + pbt - 1) / pbt) * ((L.K + 127) / 128) * p->alpha;
-    if (ctas < sms && num_kb > 1) {
-      int sp = static_cast<int>((sms + ctas - 1) / ctas);
-      if (sp > num_kb) sp = num_kb;
-      const int kbps = (num_kb + sp - 1) / sp;
-      p->fsplits = (num_kb + kbps - 1) / kbps;
+  if (p->path != kPathStaged) {
+    if (p->path == kPathFused) {
+      p->num_chunks = 1;
+      p->rows_per_chunk = p->rows_total;
+      p->chunk_tiles = p->P;
+      p->v_bytes = 0;
+    } else {  // hybrid: the whole budget goes to the V chunk (no M)
+      const size_t per_row_v =
+          static_cast<size_t>(p->nsplit) * p->a2 * p->c_pad * p->esize * p->tw;
+      long long r2 = static_cast<long long>(budget / (per_row_v ? per_row_v : 1));
+      if (r2 < 1) r2 = 1;
+      if (r2 > p->rows_total) r2 = p->rows_total;
+      p->rows_per_chunk = static_cast<int>(r2);
+      p->num_chunks = (p->rows_total + p->rows_per_chunk - 1) / p->rows_per_chunk;
+      p->chunk_tiles = static_cast<long long>(p->rows_per_chunk) * p->tw;
+      p->v_bytes = align_up(static_cast<size_t>(p->nsplit) * p->a2 * p->chunk_tiles * p->c_pad *
+                                p->esize,
+                            1024);
+    }
+    p->splits = 1;
+    if (p->num_chunks == 1) {
+      const int sms = gemm_device_sms();
+      const int num_kb = fused_num_kblocks(prec, L.C);
+      const int pbt = fused_tiles_per_unit(m);
+      const long long ctas = ((p->P + pbt - 1) / pbt) * ((L.K + 127) / 128) * p->alpha;
+      if (ctas < sms && num_kb > 1) {
+        int sp = static_cast<int>((sms + ctas - 1) / ctas);
+        if (sp > num_kb) sp = num_kb;
+        const int kbps = (num_kb + sp - 1) / sp;
+        p->fsplits = (num_kb + kbps - 1) / kbps;
+      }
     }
     if (p->fsplits > 1)
-      p->ypart_bytes = align_up(static_cast<size_t>(p->fsplits) * L.N * L.K * oh * ow * 4, 1024);
-    p->num_chunks = 1;
-    p->rows_per_chunk = p->rows_total;
-    p->chunk_tiles = p->P;
-    p->splits = 1;
-    p->v_bytes = 0;
+      p->ypart_bytes = align_up(static_cast<size_t>(p->fsplits) *
+                                    align_up(static_cast<size_t>(L.N) * L.K * oh * ow, 4) * 4,
+                                1024);
   }
-  p->m_bytes = (p->smallc || p->fused) ? 0
+  p->m_bytes = (p->smallc || p->path != kPathStaged) ? 0
                         : align_up(static_cast<size_t>(p->splits) * p->a2 * L.K * p->m_ld *
                                        p->acc_bytes,
                                    1024);
@@ -347,8 +377,11 @@ int wino_plan_get_info(wino_plan_t p, wino_plan_info_t* info) {
   info->u_bytes = p->u_bytes;
   info->workspace_bytes = p->u_bytes + p->v_bytes + p->m_bytes + p->ypart_bytes;
   info->launches_per_forward =
-      p->smallc ? 1 : (p->fused ? (p->fsplits > 1 ? 2 : 1) : p->num_chunks * 3);
-  info->fused = p->fused ? 1 : 0;
+      p->smallc ? 1
+                : p->path == kPathFused  ? 1 + (p->fsplits > 1)
+                : p->path == kPathHybrid ? p->num_chunks * 2 + (p->fsplits > 1)
+                                         : p->num_chunks * 3;
+  info->fused = p->path;
   info->fused_splits = p->fsplits;
   info->fused_small_c = p->smallc ? 1 : 0;
   info->multiplies = p->P * p->L.C * static_cast<long long>(p->L.K) * p->a2;
@@ -427,15 +460,38 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
     tm.mark(1);
     return WINO_OK;
   }
-  if (p->fused) {
-    FusedArgs fa{d, U, y, ws, p->P, L.N, L.C, L.H, L.W, L.K, L.pad, p->th, p->tw, p->oh, p->ow,
-                 p->c_pad, p->fsplits};
+  if (p->path == kPathFused) {
+    FusedArgs fa{d, U, nullptr, y, ws, p->P, 0, L.N, L.C, L.H, L.W, L.K, L.pad, p->th, p->tw,
+                 p->oh, p->ow, p->c_pad, p->fsplits};
     cudaError_t e = launch_fused(p->m, p->prec, fa, s);
     if (e != cudaSuccess) {
       if (g_err.empty()) return cuda_fail(e, "fused winograd gemm");
       return WINO_ECUDA;
     }
     tm.mark(2);
+    return WINO_OK;
+  }
+  if (p->path == kPathHybrid) {
+    void* V = ws;
+    void* yp = ws + p->v_bytes;
+    for (int ch = 0; ch < p->num_chunks; ++ch) {
+      const int row0 = ch * p->rows_per_chunk;
+      const int rows = (row0 + p->rows_per_chunk <= p->rows_total) ? p->rows_per_chunk
+                                                                    : p->rows_total - row0;
+      const long long Pc = static_cast<long long>(rows) * p->tw;
+      cudaError_t e = launch_input_transform(p->m, p->prec, d, V, L.N, L.C, L.H, L.W, L.pad,
+                                             p->th, p->tw, row0, rows, Pc, p->c_pad, s);
+      if (e != cudaSuccess) return cuda_fail(e, "input transform");
+      tm.mark(1);
+      FusedArgs fa{d, U, V, y, yp, Pc, static_cast<long long>(row0) * p->tw, L.N, L.C, L.H, L.W,
+                   L.K, L.pad, p->th, p->tw, p->oh, p->ow, p->c_pad, p->fsplits};
+      e = launch_fused(p->m, p->prec, fa, s);
+      if (e != cudaSuccess) {
+        if (g_err.empty()) return cuda_fail(e, "fused winograd gemm");
+        return WINO_ECUDA;
+      }
+      tm.mark(2);
+    }
     return WINO_OK;
   }
   void* V = ws;

@@ -77,9 +77,11 @@ int gemm_kernels_per_launch(int prec);
 struct FusedArgs {
   const void* d;  // (N,C,H,W) fp32
   const void* U;  // [nsplit][a2][K][c_pad] operand format
+  const void* V;  // NULL: form V in-kernel from d; else staged V chunk [nsplit][a2][P][c_pad]
   void* y;        // (N,K,oh,ow) fp32
   void* ypart;    // split partials (splits > 1)
-  long long P;
+  long long P;    // tiles in this launch (the chunk)
+  long long p0;   // global index of its first tile
   int N, C, H, W, K, pad, th, tw, oh, ow, c_pad;
   int splits;
 };

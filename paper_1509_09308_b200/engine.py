@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes
 import hashlib
+import os
 import threading
 from dataclasses import dataclass
 from typing import Optional, Tuple
@@ -236,7 +237,9 @@ _plans_lock = threading.Lock()
 
 
 def get_plan(cfg: LayerConfig, m: int, prec: str, workspace_limit: int = 0) -> WinogradPlan:
-    key = (cfg.N, cfg.C, cfg.H, cfg.W, cfg.K, cfg.R, cfg.S, cfg.pad, m, prec, workspace_limit)
+    # WINO_PATH (staged / fused / hybrid) is read by the C planner at plan creation
+    key = (cfg.N, cfg.C, cfg.H, cfg.W, cfg.K, cfg.R, cfg.S, cfg.pad, m, prec, workspace_limit,
+           os.environ.get("WINO_PATH", ""))
     with _plans_lock:
         plan = _plans.get(key)
         if plan is None:

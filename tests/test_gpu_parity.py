@@ -28,6 +28,18 @@ def wb():
     return wb
 
 
+# The three forward paths of the C planner (WINO_PATH, read at plan creation):
+# staged (input transform -> GEMM -> output transform), fused (one kernel),
+# hybrid (staged input transform + fused GEMM/inverse transform).
+PATHS = ["staged", "fused", "hybrid"]
+
+
+@pytest.fixture(params=PATHS)
+def path(request, monkeypatch):
+    monkeypatch.setenv("WINO_PATH", request.param)
+    return request.param
+
+
 def _run(wb, d, g, pad, m, prec=None, fx=False, cache=None):
     cfg = wb.LayerConfig(N=d.shape[0], C=d.shape[1], H=d.shape[2], W=d.shape[3], K=g.shape[0],
                          pad=pad)
@@ -37,7 +49,7 @@ def _run(wb, d, g, pad, m, prec=None, fx=False, cache=None):
 
 
 @pytest.mark.parametrize("m", [2, 4])
-def test_golden_cases_fp32(wb, golden, m):
+def test_golden_cases_fp32(wb, golden, m, path):
     for i in range(10):
         N, C, H, W, K, pad = (int(v) for v in golden[f"case{i}_shape"])
         d = O.fill_uniform((N, C, H, W), 100 + 2 * i)
@@ -65,7 +77,7 @@ def test_golden_cases_fp64(wb, golden, m):
 
 @pytest.mark.parametrize("m", [2, 4])
 @pytest.mark.parametrize("prec", ["tf32", "bf16", "fp16"])
-def test_reduced_precision_envelope(wb, golden, m, prec):
+def test_reduced_precision_envelope(wb, golden, m, prec, path):
     for i in (3, 5, 7, 9):
         N, C, H, W, K, pad = (int(v) for v in golden[f"case{i}_shape"])
         d = O.fill_uniform((N, C, H, W), 100 + 2 * i)
@@ -89,7 +101,7 @@ def test_config1_against_reference(wb, golden):
         assert abs(y.astype(np.float64).sum() - s[0]) <= 1e-6 * s[1]
 
 
-def test_zero_filters_exact(wb):
+def test_zero_filters_exact(wb, path):
     d = O.fill_uniform((1, 2, 6, 6), 1)
     g = np.zeros((2, 2, 3, 3), np.float32)
     for m in (2, 4):
@@ -97,7 +109,7 @@ def test_zero_filters_exact(wb):
             assert np.all(_run(wb, d, g, 1, m, prec=prec) == 0.0)
 
 
-def test_impulse_filter_copies_input(wb):
+def test_impulse_filter_copies_input(wb, path):
     """A centred delta filter reproduces the input: any tile-indexing or
     padding slip would show as O(1) errors.  Exact for F(2x2) (all transform
     constants are dyadic); F(4x4)'s 1/6, 1/12, 1/24 round in fp32."""
@@ -122,16 +134,17 @@ def test_fx_cache_bitwise_and_counts(wb):
     assert cache.workspace_scalars() == 36 * 4 * 8
 
 
-def test_bitwise_deterministic(wb):
+def test_bitwise_deterministic(wb, path):
     d = O.fill_uniform((1, 8, 9, 9), 9)
     g = O.fill_uniform((4, 8, 3, 3), 10)
     for prec in ("fp32", "bf16"):
         assert np.array_equal(_run(wb, d, g, 1, 2, prec=prec), _run(wb, d, g, 1, 2, prec=prec))
 
 
-def test_chunked_planner_matches_single_chunk(wb):
+def test_chunked_planner_matches_single_chunk(wb, monkeypatch):
     """Workspace-limited plans (many row chunks) give bit-identical outputs."""
     import torch
+    monkeypatch.setenv("WINO_PATH", "staged")
     cfg = wb.LayerConfig(N=2, C=16, H=30, W=22, K=24, pad=1)
     d = torch.from_numpy(O.fill_uniform((2, 16, 30, 22), 3)).cuda()
     g = torch.from_numpy(O.fill_uniform((24, 16, 3, 3), 4)).cuda()
@@ -145,7 +158,7 @@ def test_chunked_planner_matches_single_chunk(wb):
         assert torch.equal(ya, yb)
 
 
-def test_random_shape_sweep(wb, golden):
+def test_random_shape_sweep(wb, golden, path):
     """First 40 shapes of the acceptance sweep (test_acceptance.py:120-142)."""
     shapes = golden["sweep55_shapes"][:40]
     worst = {2: 0.0, 4: 0.0}
@@ -172,13 +185,18 @@ def test_grad_inputs_matches_oracle(wb):
 
 
 @pytest.mark.parametrize("m,prec", [(2, "fp32"), (4, "fp32"), (4, "bf16"), (2, "tf32")])
-def test_split_c_small_p_layer(wb, m, prec):
+def test_split_c_small_p_layer(wb, m, prec, path):
     """conv5-like small-P layer: the planner splits the channel reduction across
-    CTAs; the output transform must re-assemble it exactly."""
+    CTAs (staged: M slices summed by the output transform; fused/hybrid: partial
+    y slices summed in split order); the result must re-assemble exactly."""
     import torch
     cfg = wb.LayerConfig(N=1, C=512, H=14, W=14, K=256, pad=1)
     plan = wb.WinogradPlan(cfg, m, prec)
-    assert plan.info["gemm_splits"] > 1
+    assert plan.info["fused"] == PATHS.index(path)
+    if path == "staged":
+        assert plan.info["gemm_splits"] > 1
+    else:
+        assert plan.info["fused_splits"] > 1
     d = O.fill_uniform((1, 512, 14, 14), 31)
     g = O.fill_uniform((256, 512, 3, 3), 32)
     y = plan.forward(torch.from_numpy(d).cuda(), g=torch.from_numpy(g).cuda()).cpu().numpy()
@@ -189,3 +207,23 @@ def test_split_c_small_p_layer(wb, m, prec):
         assert np.abs(y - yo).max() <= 2e-5 * (1 + np.abs(yo).max())
     else:
         assert O.max_abs_error(y, ref) / np.abs(ref).max() <= REL_TOL[(prec, m)]
+
+
+def test_hybrid_chunked_matches_oracle(wb, monkeypatch):
+    """Hybrid path with a workspace that forces many V row chunks (the fused
+    kernel's tile offset p0 and the chunk-local V map): same result as one chunk
+    up to summation order, and within the fp32 gate of the reference."""
+    import torch
+    monkeypatch.setenv("WINO_PATH", "hybrid")
+    cfg = wb.LayerConfig(N=2, C=40, H=30, W=22, K=24, pad=1)
+    dn = O.fill_uniform((2, 40, 30, 22), 13)
+    gn = O.fill_uniform((24, 40, 3, 3), 14)
+    d, g = torch.from_numpy(dn).cuda(), torch.from_numpy(gn).cuda()
+    ref = O.direct_forward(dn, gn, 1)
+    for m in (2, 4):
+        small = wb.WinogradPlan(cfg, m, "fp32", workspace_limit=256 * 1024)
+        assert small.info["fused"] == 2 and small.info["num_chunks"] > 2
+        y = small.forward(d, g=g).cpu().numpy()
+        assert O.max_abs_error(y, ref) < (5e-4 if m == 2 else 5e-3)
+        yo = O.winograd_forward(dn, gn, m, 1)
+        assert np.abs(y - yo).max() <= 2e-5 * (1 + np.abs(yo).max())

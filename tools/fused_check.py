@@ -46,8 +46,8 @@ def main():
         for m in (2, 4):
             for prec in PRECS:
                 try:
-                    yf, info = run(cfg, m, prec, d, g, "auto")
-                    yu, _ = run(cfg, m, prec, d, g, "unfused")
+                    yf, info = run(cfg, m, prec, d, g, os.environ.get("CHECK_PATH", "fused"))
+                    yu, _ = run(cfg, m, prec, d, g, "staged")
                 except Exception as e:  # noqa: BLE001
                     print(f"{(N, C, H, W, K, pad)} F{m} {prec}: ERROR {e}")
                     bad += 1
