@@ -429,6 +429,33 @@ struct StageTimer {
 };
 }  // namespace
 
+// Side stream on which the filter transform runs concurrently with the input
+// transform (independent stages; the GEMM joins both).  One per host thread
+// and device, created on first use; under stream capture the record/wait pair
+// becomes a graph fork/join.
+namespace {
+struct SideStream {
+  cudaStream_t st = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream* side_stream() {
+  constexpr int kMaxDev = 64;
+  thread_local SideStream ss[kMaxDev];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return nullptr;
+  SideStream& x = ss[dev];
+  if (!x.st) {
+    if (cudaStreamCreateWithFlags(&x.st, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming) != cudaSuccess) {
+      x.st = nullptr;
+      return nullptr;
+    }
+  }
+  return &x;
+}
+}  // namespace
+
 static int forward_impl(wino_plan_t p, const void* d, const void* U, const void* g, void* y,
                         void* workspace, size_t workspace_bytes, void* stream,
                         wino_timer_s* timer) {
@@ -445,13 +472,36 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
     set_error("workspace too small: %zu < %zu bytes", workspace_bytes, need);
     return WINO_EINVAL;
   }
+  // non-FX: G g G^T into the workspace.  Unless stage-timed, it runs on the
+  // side stream alongside the input transform and is joined before the GEMM.
+  SideStream* side = nullptr;
   if (!U) {
-    cudaError_t e = launch_filter_transform(p->m, p->prec, g, ws, p->L.K, p->L.C, p->c_pad, s);
+    cudaStream_t fs = s;
+    if (!timer && !p->smallc && p->path != kPathFused && getenv("WINO_NO_OVERLAP") == nullptr)
+      side = side_stream();
+    if (side) {
+      if (cudaEventRecord(side->fork, s) != cudaSuccess ||
+          cudaStreamWaitEvent(side->st, side->fork, 0) != cudaSuccess)
+        side = nullptr;
+      else
+        fs = side->st;
+    }
+    cudaError_t e = launch_filter_transform(p->m, p->prec, g, ws, p->L.K, p->L.C, p->c_pad, fs);
     if (e != cudaSuccess) return cuda_fail(e, "filter transform");
+    if (side) {
+      e = cudaEventRecord(side->join, side->st);
+      if (e != cudaSuccess) return cuda_fail(e, "filter transform join");
+    }
     tm.mark(0);
     U = ws;
     ws += p->u_bytes;
   }
+  auto join_filters = [&]() -> cudaError_t {
+    if (!side) return cudaSuccess;
+    cudaError_t e = cudaStreamWaitEvent(s, side->join, 0);
+    side = nullptr;
+    return e;
+  };
   const wino_layer_t& L = p->L;
   if (p->smallc) {
     cudaError_t e = launch_fused_smallc(p->m, p->prec, d, U, y, L.N, L.C, L.H, L.W, L.K, L.pad,
@@ -485,6 +535,8 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
       tm.mark(1);
       FusedArgs fa{d, U, V, y, yp, Pc, static_cast<long long>(row0) * p->tw, L.N, L.C, L.H, L.W,
                    L.K, L.pad, p->th, p->tw, p->oh, p->ow, p->c_pad, p->fsplits};
+      e = join_filters();
+      if (e != cudaSuccess) return cuda_fail(e, "filter transform join");
       e = launch_fused(p->m, p->prec, fa, s);
       if (e != cudaSuccess) {
         if (g_err.empty()) return cuda_fail(e, "fused winograd gemm");
@@ -506,6 +558,8 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
     if (e != cudaSuccess) return cuda_fail(e, "input transform");
     tm.mark(1);
     GemmArgs ga{V, U, Mb, p->a2, L.K, L.C, p->c_pad, Pc, p->bn, p->splits, p->m_ld};
+    e = join_filters();
+    if (e != cudaSuccess) return cuda_fail(e, "filter transform join");
     e = launch_batched_gemm(p->prec, ga, s);
     if (e != cudaSuccess) {
       if (g_err.empty()) return cuda_fail(e, "batched gemm");
