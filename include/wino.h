@@ -121,6 +121,19 @@ int wino_forward_timed(wino_plan_t plan, const void* d, const void* U, const voi
                        void* workspace, size_t workspace_bytes, void* stream, wino_timer_t timer);
 
 /* Last error message of the calling thread ("" if none). */
+/* Weight gradient dL/dg by the F(3x3, 2x2) decomposition; replaces
+ * winoconv.engine.winograd_grad_weights (engine.py:278-328).
+ * d: (N,C,H,W), dy: (N,K,out_h,out_w), dg: (K,C,3,3) -- device pointers in the
+ * data type (fp32, or fp64 for WINO_PREC_FP64).  R == S == 3 (else
+ * WINO_EUNSUPPORTED, the reference's ValueError).  workspace_limit bounds the
+ * tile-chunk staging (0 = default); wino_wgrad_workspace returns the bytes a
+ * call with the same arguments needs.  Enqueued on `stream`. */
+int wino_wgrad_workspace(const wino_layer_t* layer, int prec, size_t workspace_limit,
+                         size_t* bytes);
+int wino_grad_weights(const wino_layer_t* layer, int prec, const void* d, const void* dy,
+                      void* dg, void* workspace, size_t workspace_bytes, size_t workspace_limit,
+                      void* stream);
+
 const char* wino_last_error(void);
 /* Library version string. */
 const char* wino_version(void);

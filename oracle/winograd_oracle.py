@@ -325,6 +325,56 @@ def direct_forward(d: np.ndarray, g: np.ndarray, pad: int,
     return y
 
 
+def direct_grad_weights(d: np.ndarray, dy: np.ndarray, pad: int, R: int = 3, S: int = 3,
+                        accum=np.float64) -> np.ndarray:
+    """dG[k,c,u,v] = sum_i sum_{x,y} d[i,c,x+u-pad,y+v-pad] * dy[i,k,x,y]
+    (direct.py:149-177): the fp64 ground truth of the weight gradient."""
+    N, C, H, W = d.shape
+    _, K, oh, ow = dy.shape
+    da = d.astype(accum, copy=False)
+    ya = dy.astype(accum, copy=False)
+    dg = np.zeros((K, C, R, S), dtype=accum)
+    for u in range(R):
+        for v in range(S):
+            ro, co = u - pad, v - pad
+            xs, xe = max(0, -ro), min(oh, H - ro)
+            ys, ye = max(0, -co), min(ow, W - co)
+            if xs >= xe or ys >= ye:
+                continue
+            win = da[:, :, xs + ro:xe + ro, ys + co:ye + co]
+            dg[:, :, u, v] = np.einsum("ichw,ikhw->kc", win, ya[:, :, xs:xe, ys:ye])
+    return dg
+
+
+def winograd_grad_weights(d: np.ndarray, dy: np.ndarray, pad: int) -> np.ndarray:
+    """dL/dg via F(3x3, 2x2) (engine.py:278-328).
+
+    dy is cut into non-overlapping 2x2 tiles (zero-filled past the output
+    edge); each pairs with the 4x4 input patch at (2ty - pad, 2tx - pad).
+    Uw = G dy_tile G^T (alpha^2, K, B), Vw = B^T d_tile B (alpha^2, B, C),
+    M = Uw @ Vw per component (reduction over tiles B), dg = A^T M A.
+    Arithmetic in the input dtype, as the reference.
+    """
+    if d.dtype != dy.dtype:
+        raise ValueError("mixed precisions")
+    N, C, H, W = d.shape
+    _, K, oh, ow = dy.shape
+    BT, G, AT = lowered(3, 2, d.dtype)
+    mw, aw = 2, 4
+    gh, gw = -(-oh // mw), -(-ow // mw)
+    B = N * gh * gw
+    yt = gather_tiles(dy, gh, gw, mw, mw, 0).reshape(B, K, mw, mw)
+    dt = gather_tiles(d, gh, gw, mw, aw, pad).reshape(B, C, aw, aw)
+    t = np.einsum("xr,bkrs->xbks", G, yt)
+    Uw = np.ascontiguousarray(np.einsum("ys,xbks->xykb", G, t).reshape(aw * aw, K, B))
+    t = np.einsum("xu,bcuv->xbcv", BT, dt)
+    Vw = np.ascontiguousarray(np.einsum("yv,xbcv->xybc", BT, t).reshape(aw * aw, B, C))
+    M = batched_matmul(Uw, Vw)
+    M4 = M.reshape(aw, aw, K, C)
+    t2 = np.einsum("mx,xykc->mykc", AT, M4)
+    return np.ascontiguousarray(np.einsum("ny,mykc->kcmn", AT, t2))
+
+
 def gflops_direct(N, C, H, W, K, pad, R=3, S=3, depth=1) -> float:
     """2*N*C*K*outH*outW*R*S / 1e9 * depth (direct.py:179-183)."""
     oh, ow = out_dims(H, W, R, S, pad)

@@ -9,7 +9,8 @@ fails loudly if it is missing: there is no CPU fallback.
 from ._lib import version  # noqa: F401  (loads libwino.so or raises)
 from .commands import BENCH_ALGOS, cmd_bench, layer_inputs, parse_algo, run_layer
 from .engine import (FilterCache, TileGrid, WinogradPlan, get_plan, multiply_stage_flops,
-                     shared_filter_cache, tile_count, winograd_forward, winograd_grad_inputs)
+                     shared_filter_cache, tile_count, winograd_forward, winograd_grad_inputs,
+                     winograd_grad_weights, grad_weights_device)
 from .layer import LayerConfig, OpCounter, WinogradAlgorithm, builtin, builtin_sizes, gflops_direct
 from .suites import LayerSuite, get_suite, vgg_e, vgg_e_accuracy
 from .tensors import Precision, Tensor4, fill_uniform, max_abs_error, quantize_fp16
@@ -20,7 +21,7 @@ __all__ = [
     "Precision", "Tensor4", "fill_uniform", "quantize_fp16", "max_abs_error",
     "LayerConfig", "gflops_direct", "WinogradAlgorithm", "builtin", "builtin_sizes",
     "OpCounter", "FilterCache", "TileGrid", "tile_count", "multiply_stage_flops",
-    "winograd_forward", "winograd_grad_inputs", "shared_filter_cache", "WinogradPlan",
+    "winograd_forward", "winograd_grad_inputs", "winograd_grad_weights", "grad_weights_device", "shared_filter_cache", "WinogradPlan",
     "get_plan", "run_layer", "cmd_bench", "layer_inputs", "parse_algo", "BENCH_ALGOS",
     "LayerSuite", "get_suite", "vgg_e", "vgg_e_accuracy", "version", "__version__",
 ]

@@ -239,7 +239,14 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
   if (prec == kFP32) bn = 128;  // 3 split stages of 64 KB fit; 256 would leave 2
   while (bn > 32 && bn / 2 >= L.K) bn /= 2;
   const long long ptiles = (p->P + 127) / 128;
-  while (bn > 64 && ptiles * ((L.K + bn - 1) / bn) * p->a2 < 148) bn /= 2;
+  // 3xTF32 streams twice the operand bytes: keep 128-wide tiles (less V
+  // re-reading) and let split-C fill the SMs (measured: VGG-E N=1 -4%).
+  const int bn_floor = prec == kFP32 ? 128 : 64;
+  while (bn > bn_floor && ptiles * ((L.K + bn - 1) / bn) * p->a2 < 148) bn /= 2;
+  if (const char* e = getenv("WINO_GEMM_BN")) {  // tuning override (32/64/128/256)
+    const int v = atoi(e);
+    if (v == 32 || v == 64 || v == 128 || v == 256) bn = v;
+  }
   p->bn = bn;
 
   p->smallc = L.C <= kSmallCMax;
@@ -660,6 +667,155 @@ int wino_forward_host(wino_plan_t p, const void* d_host, const void* U, const vo
   if (rc != WINO_OK) return rc;
   e = cudaMemcpyAsync(y_host, y_dev, yb, cudaMemcpyDeviceToHost, s);
   if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
+  return WINO_OK;
+}
+
+// ---------------------------------------------------------------- weight gradient
+// dL/dg via F(3x3, 2x2) (engine.py:278-328): transforms of dY tiles (Uw) and
+// input patches (Vw) with the tile index innermost, the 16 tile-reduction
+// GEMMs on the same tcgen05 kernel as the forward (reduction axis = tiles),
+// and one inverse transform per (k, c).  Tiles are processed in chunks that
+// fit the workspace budget; every chunk x split writes its own M slice and the
+// inverse transform sums the slices in order (deterministic).
+namespace {
+struct WgPlan {
+  int oh, ow, gh, gw;
+  long long B, nb, b_pad;
+  int nchunks, esize, nsplit, acc_bytes, bn, splits;
+  long long m_ld;
+  size_t u_bytes, v_bytes, m_bytes;
+};
+constexpr size_t kWgradDefaultWorkspace = 256ull << 20;
+
+int wgrad_plan(const wino_layer_t* layer, int prec, size_t limit, WgPlan* w) {
+  if (!layer) {
+    set_error("null argument");
+    return WINO_EINVAL;
+  }
+  const wino_layer_t& L = *layer;
+  if (L.N < 1 || L.C < 1 || L.H < 1 || L.W < 1 || L.K < 1 || L.R < 1 || L.S < 1 || L.pad < 0) {
+    set_error("N, C, H, W, K, R, S must be >= 1 and pad >= 0");
+    return WINO_EINVAL;
+  }
+  if (L.R != 3 || L.S != 3) {  // engine.py:292-295
+    set_error("default weight-gradient algorithm needs R=S=3, got %dx%d", L.R, L.S);
+    return WINO_EUNSUPPORTED;
+  }
+  if (prec < WINO_PREC_FP32 || prec > WINO_PREC_FP64) {
+    set_error("unknown precision %d", prec);
+    return WINO_EINVAL;
+  }
+  w->oh = L.H + 2 * L.pad - 2;
+  w->ow = L.W + 2 * L.pad - 2;
+  if (w->oh < 1 || w->ow < 1) {
+    set_error("output dimensions must be >= 1");
+    return WINO_EINVAL;
+  }
+  w->gh = (w->oh + 1) / 2;
+  w->gw = (w->ow + 1) / 2;
+  w->B = static_cast<long long>(L.N) * w->gh * w->gw;
+  w->esize = op_bytes(prec);
+  w->nsplit = op_splits(prec);
+  w->acc_bytes = prec == kFP64 ? 8 : 4;
+  const size_t budget = limit ? limit : kWgradDefaultWorkspace;
+  const size_t per_tile = static_cast<size_t>(w->nsplit) * 16 * (L.K + L.C) * w->esize;
+  long long nb = static_cast<long long>(budget / per_tile);
+  if (nb < 64) nb = 64;
+  if (nb >= w->B) nb = w->B;
+  else nb = nb / 64 * 64;
+  w->nb = nb;
+  w->nchunks = static_cast<int>((w->B + nb - 1) / nb);
+  w->b_pad = static_cast<long long>(align_up(static_cast<size_t>(nb), 16 / w->esize));
+  int bn = prec == kFP32 ? 128 : 256;
+  while (bn > 32 && bn / 2 >= L.K) bn /= 2;
+  w->bn = bn;
+  w->splits = 1;
+  if (prec != kFP64) {
+    const int num_kb = gemm_num_kblocks(prec, static_cast<int>(nb));
+    const long long units = ((L.C + 127) / 128) * ((L.K + bn - 1) / bn) * 16LL;
+    const long long target = 2LL * gemm_device_sms();
+    if (units < target && num_kb >= 4) {
+      long long sp = (target + units - 1) / units;
+      if (sp > num_kb / 2) sp = num_kb / 2;
+      const int kbps = static_cast<int>((num_kb + sp - 1) / sp);
+      w->splits = (num_kb + kbps - 1) / kbps;
+    }
+  }
+  w->m_ld = static_cast<long long>(align_up(static_cast<size_t>(L.C), 4));
+  w->u_bytes = align_up(static_cast<size_t>(w->nsplit) * 16 * L.K * w->b_pad * w->esize, 1024);
+  w->v_bytes = align_up(static_cast<size_t>(w->nsplit) * 16 * L.C * w->b_pad * w->esize, 1024);
+  // one chunk's split slices, plus a running accumulator when there are
+  // several chunks (folded after every chunk: bounded memory, fixed order)
+  w->m_bytes = align_up(static_cast<size_t>(w->splits + (w->nchunks > 1 ? 1 : 0)) * 16 * L.K *
+                            w->m_ld * w->acc_bytes,
+                        1024);
+  return WINO_OK;
+}
+}  // namespace
+
+int wino_wgrad_workspace(const wino_layer_t* layer, int prec, size_t workspace_limit,
+                         size_t* bytes) {
+  g_err.clear();
+  if (!bytes) {
+    set_error("null argument");
+    return WINO_EINVAL;
+  }
+  WgPlan w;
+  const int rc = wgrad_plan(layer, prec, workspace_limit, &w);
+  if (rc != WINO_OK) return rc;
+  *bytes = w.u_bytes + w.v_bytes + w.m_bytes;
+  return WINO_OK;
+}
+
+int wino_grad_weights(const wino_layer_t* layer, int prec, const void* d, const void* dy,
+                      void* dg, void* workspace, size_t workspace_bytes, size_t workspace_limit,
+                      void* stream) {
+  g_err.clear();
+  if (!d || !dy || !dg || !workspace) {
+    set_error("null argument");
+    return WINO_EINVAL;
+  }
+  WgPlan w;
+  int rc = wgrad_plan(layer, prec, workspace_limit, &w);
+  if (rc != WINO_OK) return rc;
+  if (workspace_bytes < w.u_bytes + w.v_bytes + w.m_bytes) {
+    set_error("workspace too small: %zu < %zu bytes", workspace_bytes,
+              w.u_bytes + w.v_bytes + w.m_bytes);
+    return WINO_EINVAL;
+  }
+  const wino_layer_t& L = *layer;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  unsigned char* ws = static_cast<unsigned char*>(workspace);
+  void* Uw = ws;
+  void* Vw = ws + w.u_bytes;
+  unsigned char* Mb = ws + w.u_bytes + w.v_bytes;
+  const size_t slice = static_cast<size_t>(16) * L.K * w.m_ld * w.acc_bytes;
+  unsigned char* acc = Mb;                                   // running sum (several chunks)
+  unsigned char* parts = w.nchunks > 1 ? Mb + slice : Mb;    // this chunk's split slices
+  for (int ch = 0; ch < w.nchunks; ++ch) {
+    const long long b0 = static_cast<long long>(ch) * w.nb;
+    const long long nb = (b0 + w.nb <= w.B) ? w.nb : w.B - b0;
+    cudaError_t e = launch_wgrad_transforms(prec, d, dy, Uw, Vw, L.K, L.C, L.H, L.W, L.pad, w.oh,
+                                            w.ow, w.gh, w.gw, b0, nb, w.b_pad, s);
+    if (e != cudaSuccess) return cuda_fail(e, "weight-gradient transforms");
+    // M[comp][k][c] = sum_b Uw[comp][k][b] Vw[comp][c][b]: the forward GEMM with
+    // (rows = C, reduction = tiles), partial sums in `splits` slices
+    GemmArgs ga{Vw, Uw, parts, 16, L.K, static_cast<int>(nb), static_cast<int>(w.b_pad), L.C,
+                w.bn, w.splits, w.m_ld};
+    e = launch_batched_gemm(prec, ga, s);
+    if (e != cudaSuccess) {
+      if (g_err.empty()) return cuda_fail(e, "weight-gradient gemm");
+      return WINO_ECUDA;
+    }
+    if (w.nchunks > 1) {
+      e = launch_wgrad_accumulate(prec, acc, parts, static_cast<long long>(16) * L.K * w.m_ld,
+                                  w.splits, ch == 0 ? 1 : 0, s);
+      if (e != cudaSuccess) return cuda_fail(e, "weight-gradient accumulate");
+    }
+  }
+  cudaError_t e = launch_wgrad_inverse(prec, Mb, dg, L.K, L.C, w.m_ld,
+                                       w.nchunks > 1 ? 1 : w.splits, s);
+  if (e != cudaSuccess) return cuda_fail(e, "weight-gradient inverse transform");
   return WINO_OK;
 }
 

@@ -54,6 +54,19 @@ cudaError_t launch_fused_smallc(int m, int prec, const void* d, const void* U, v
                                 int C, int H, int W, int K, int pad, int th, int tw, int oh,
                                 int ow, int c_pad, cudaStream_t s);
 
+// Weight gradient F(3x3,2x2) (engine.py:278-328): transforms of tiles
+// [b0, b0+nb) into Uw [nsplit][16][K][b_pad] and Vw [nsplit][16][C][b_pad]
+// (tile index innermost), and the inverse transform of the summed M slices
+// [slices][16][K][m_ld] into dg (K,C,3,3).
+cudaError_t launch_wgrad_transforms(int prec, const void* d, const void* dy, void* Uw, void* Vw,
+                                    int K, int C, int H, int W, int pad, int oh, int ow, int gh,
+                                    int gw, long long b0, long long nb, long long b_pad,
+                                    cudaStream_t s);
+cudaError_t launch_wgrad_accumulate(int prec, void* acc, const void* slices, long long n,
+                                    int splits, int first, cudaStream_t s);
+cudaError_t launch_wgrad_inverse(int prec, const void* Mbuf, void* dg, int K, int C,
+                                 long long m_ld, int slices, cudaStream_t s);
+
 struct GemmArgs {
   const void* V;   // [nsplit][a2][Pc][c_pad]
   const void* U;   // [nsplit][a2][K][c_pad]

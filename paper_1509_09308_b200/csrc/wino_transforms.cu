@@ -758,4 +758,188 @@ cudaError_t launch_fused_smallc(int m, int prec, const void* d, const void* U, v
                 : smallc_dispatch<4>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
 }
 
+// ====================================================== weight gradient
+// F(3x3, 2x2) (engine.py:278-328): dY is cut into non-overlapping 2x2 tiles
+// (zero past the output edge), each paired with the 4x4 input patch at
+// (2ty - pad, 2tx - pad).  The tile index b is the GEMM reduction axis, so
+// both transforms store b innermost (the K-major operand layout of the
+// tcgen05 GEMM):  Uw[s][comp][k][b] = (G y G^T),  Vw[s][comp][c][b] = (B^T d B).
+// Thread = (row k or c, tile b), b fastest: coalesced stores.
+
+template <int PREC>
+__global__ void __launch_bounds__(256) wgrad_dy_transform_kernel(
+    const typename OpStore<PREC>::T* __restrict__ dy, void* __restrict__ Uw, int K, int oh,
+    int ow, int gh, int gw, long long b0, long long nb, long long b_pad) {
+  using T = typename OpStore<PREC>::T;
+  griddep_launch();
+  griddep_wait();
+  const long long bl = static_cast<long long>(blockIdx.x) * 256 + threadIdx.x;
+  const int k = blockIdx.y;
+  if (bl >= nb) return;
+  const long long b = b0 + bl;
+  const long long per_img = static_cast<long long>(gh) * gw;
+  const int n = static_cast<int>(b / per_img);
+  const int rem = static_cast<int>(b - n * per_img);
+  const int ty = rem / gw, tx = rem - (rem / gw) * gw;
+  const T* src = dy + ((static_cast<long long>(n) * K + k) * oh + 2 * ty) * ow + 2 * tx;
+  T in[2][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      in[i][j] = (2 * ty + i < oh && 2 * tx + j < ow) ? src[i * ow + j] : T(0);
+  T out[4][4];
+  sandwich<T, 4, 2>(in, out, [](int i, int j) { return Alg32::G(i, j); });
+  const size_t plane = static_cast<size_t>(16) * K * b_pad;
+  size_t idx = static_cast<size_t>(k) * b_pad + bl;
+#pragma unroll
+  for (int xi = 0; xi < 4; ++xi)
+#pragma unroll
+    for (int nu = 0; nu < 4; ++nu) {
+      OpStore<PREC>::put(Uw, idx, plane, out[xi][nu]);
+      idx += static_cast<size_t>(K) * b_pad;
+    }
+}
+
+template <int PREC>
+__global__ void __launch_bounds__(256) wgrad_d_transform_kernel(
+    const typename OpStore<PREC>::T* __restrict__ d, void* __restrict__ Vw, int C, int H, int W,
+    int pad, int gh, int gw, long long b0, long long nb, long long b_pad) {
+  using T = typename OpStore<PREC>::T;
+  griddep_launch();
+  griddep_wait();
+  const long long bl = static_cast<long long>(blockIdx.x) * 256 + threadIdx.x;
+  const int c = blockIdx.y;
+  if (bl >= nb) return;
+  const long long b = b0 + bl;
+  const long long per_img = static_cast<long long>(gh) * gw;
+  const int n = static_cast<int>(b / per_img);
+  const int rem = static_cast<int>(b - n * per_img);
+  const int ty = rem / gw, tx = rem - (rem / gw) * gw;
+  const int y0 = 2 * ty - pad, x0 = 2 * tx - pad;
+  const T* plane_in = d + (static_cast<long long>(n) * C + c) * H * W;
+  T in[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int yy = y0 + u, xx = x0 + v;
+      in[u][v] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? plane_in[yy * W + xx] : T(0);
+    }
+  T out[4][4];
+  sandwich<T, 4, 4>(in, out, [](int i, int j) { return Alg32::BT(i, j); });
+  const size_t plane = static_cast<size_t>(16) * C * b_pad;
+  size_t idx = static_cast<size_t>(c) * b_pad + bl;
+#pragma unroll
+  for (int xi = 0; xi < 4; ++xi)
+#pragma unroll
+    for (int nu = 0; nu < 4; ++nu) {
+      OpStore<PREC>::put(Vw, idx, plane, out[xi][nu]);
+      idx += static_cast<size_t>(C) * b_pad;
+    }
+}
+
+// dg[k][c] = A^T (sum_s M[s][.][k][c]) A, slices summed in ascending order.
+template <typename TA>
+__global__ void __launch_bounds__(256) wgrad_inverse_kernel(const TA* __restrict__ Mbuf,
+                                                            TA* __restrict__ dg, int K, int C,
+                                                            long long m_ld, int slices) {
+  griddep_launch();
+  griddep_wait();
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  const int k = blockIdx.y;
+  if (c >= C) return;
+  const size_t comp_stride = static_cast<size_t>(K) * m_ld;
+  TA acc[4][4];
+#pragma unroll
+  for (int xi = 0; xi < 4; ++xi)
+#pragma unroll
+    for (int nu = 0; nu < 4; ++nu)
+      acc[xi][nu] = Mbuf[(xi * 4 + nu) * comp_stride + static_cast<size_t>(k) * m_ld + c];
+  for (int s = 1; s < slices; ++s) {
+    const TA* Ms = Mbuf + static_cast<size_t>(s) * 16 * comp_stride;
+#pragma unroll
+    for (int xi = 0; xi < 4; ++xi)
+#pragma unroll
+      for (int nu = 0; nu < 4; ++nu)
+        acc[xi][nu] += Ms[(xi * 4 + nu) * comp_stride + static_cast<size_t>(k) * m_ld + c];
+  }
+  TA out[3][3];
+  sandwich<TA, 3, 4>(acc, out, [](int i, int j) { return Alg32::AT(i, j); });
+  TA* dst = dg + (static_cast<size_t>(k) * C + c) * 9;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) dst[i * 3 + j] = out[i][j];
+}
+
+// acc (+)= sum_s slice[s], ascending s (one tile chunk's split partials).
+template <typename TA>
+__global__ void __launch_bounds__(256) wgrad_accumulate_kernel(TA* __restrict__ acc,
+                                                               const TA* __restrict__ slices,
+                                                               long long n, int splits,
+                                                               int first) {
+  griddep_launch();
+  griddep_wait();
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += 256LL * gridDim.x) {
+    TA v = first ? slices[i] : acc[i] + slices[i];
+    for (int s = 1; s < splits; ++s) v += slices[s * n + i];
+    acc[i] = v;
+  }
+}
+
+cudaError_t launch_wgrad_accumulate(int prec, void* acc, const void* slices, long long n,
+                                    int splits, int first, cudaStream_t s) {
+  long long blocks = (n + 255) / 256;
+  if (blocks > 8 * 148) blocks = 8 * 148;
+  const dim3 grid(static_cast<unsigned>(blocks > 0 ? blocks : 1));
+  if (prec == kFP64)
+    launch_k(wgrad_accumulate_kernel<double>, grid, dim3(256), 0, s, static_cast<double*>(acc),
+             static_cast<const double*>(slices), n, splits, first);
+  else
+    launch_k(wgrad_accumulate_kernel<float>, grid, dim3(256), 0, s, static_cast<float*>(acc),
+             static_cast<const float*>(slices), n, splits, first);
+  return cudaGetLastError();
+}
+
+template <int PREC>
+static cudaError_t wgrad_tf_one(const void* d, const void* dy, void* Uw, void* Vw, int K, int C,
+                                int H, int W, int pad, int oh, int ow, int gh, int gw,
+                                long long b0, long long nb, long long b_pad, cudaStream_t s) {
+  using T = typename OpStore<PREC>::T;
+  const unsigned gx = static_cast<unsigned>((nb + 255) / 256);
+  launch_k(wgrad_dy_transform_kernel<PREC>, dim3(gx, K), dim3(256), 0, s,
+           static_cast<const T*>(dy), Uw, K, oh, ow, gh, gw, b0, nb, b_pad);
+  launch_k(wgrad_d_transform_kernel<PREC>, dim3(gx, C), dim3(256), 0, s,
+           static_cast<const T*>(d), Vw, C, H, W, pad, gh, gw, b0, nb, b_pad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wgrad_transforms(int prec, const void* d, const void* dy, void* Uw, void* Vw,
+                                    int K, int C, int H, int W, int pad, int oh, int ow, int gh,
+                                    int gw, long long b0, long long nb, long long b_pad,
+                                    cudaStream_t s) {
+  if (nb <= 0) return cudaSuccess;
+  switch (prec) {
+    case kFP32: return wgrad_tf_one<kFP32>(d, dy, Uw, Vw, K, C, H, W, pad, oh, ow, gh, gw, b0, nb, b_pad, s);
+    case kTF32: return wgrad_tf_one<kTF32>(d, dy, Uw, Vw, K, C, H, W, pad, oh, ow, gh, gw, b0, nb, b_pad, s);
+    case kBF16: return wgrad_tf_one<kBF16>(d, dy, Uw, Vw, K, C, H, W, pad, oh, ow, gh, gw, b0, nb, b_pad, s);
+    case kFP16: return wgrad_tf_one<kFP16>(d, dy, Uw, Vw, K, C, H, W, pad, oh, ow, gh, gw, b0, nb, b_pad, s);
+    case kFP64: return wgrad_tf_one<kFP64>(d, dy, Uw, Vw, K, C, H, W, pad, oh, ow, gh, gw, b0, nb, b_pad, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_wgrad_inverse(int prec, const void* Mbuf, void* dg, int K, int C,
+                                 long long m_ld, int slices, cudaStream_t s) {
+  const dim3 grid((C + 255) / 256, K);
+  if (prec == kFP64)
+    launch_k(wgrad_inverse_kernel<double>, grid, dim3(256), 0, s,
+             static_cast<const double*>(Mbuf), static_cast<double*>(dg), K, C, m_ld, slices);
+  else
+    launch_k(wgrad_inverse_kernel<float>, grid, dim3(256), 0, s, static_cast<const float*>(Mbuf),
+             static_cast<float*>(dg), K, C, m_ld, slices);
+  return cudaGetLastError();
+}
+
 }  // namespace wino

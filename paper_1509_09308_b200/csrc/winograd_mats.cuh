@@ -55,6 +55,24 @@ struct Alg<4> {
   }
 };
 
+// F(3,2) (winograd.py:171-189): the weight-gradient algorithm F(3x3, 2x2)
+// (engine.py:278-328).  BT is 4x4, G is 4x2 (applied to 2x2 dY tiles), AT 3x4.
+struct Alg32 {
+  static constexpr int m = 3, r = 2, alpha = 4;
+  __host__ __device__ static constexpr double BT(int i, int j) {
+    constexpr double t[4][4] = {{1, 0, -1, 0}, {0, 1, 1, 0}, {0, -1, 1, 0}, {0, -1, 0, 1}};
+    return t[i][j];
+  }
+  __host__ __device__ static constexpr double G(int i, int j) {
+    constexpr double t[4][2] = {{1, 0}, {0.5, 0.5}, {0.5, -0.5}, {0, 1}};
+    return t[i][j];
+  }
+  __host__ __device__ static constexpr double AT(int i, int j) {
+    constexpr double t[3][4] = {{1, 1, 1, 0}, {0, 1, -1, 0}, {0, 1, 1, 1}};
+    return t[i][j];
+  }
+};
+
 // acc + c*x with the coefficient folded at compile time.
 template <typename T>
 __device__ __forceinline__ T mac(T acc, double c, T x, bool first) {

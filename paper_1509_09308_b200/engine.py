@@ -386,3 +386,70 @@ def winograd_grad_inputs(dy, g, cfg: LayerConfig, alg: Optional[WinogradAlgorith
     if tuple(dd.shape) != (cfg.N, cfg.C, cfg.H, cfg.W):
         raise AssertionError(f"input gradient came out {dd.shape}")
     return dd
+
+
+# --------------------------------------------------------------------- dL/dg
+
+def grad_weights_device(d, dy, cfg: LayerConfig, prec: str = "fp32", workspace=None,
+                        workspace_limit: int = 0, stream=None):
+    """Device-level weight gradient (C ABI ``wino_grad_weights``): d (N,C,H,W)
+    and dy (N,K,out_h,out_w) CUDA tensors -> dg (K,C,3,3) CUDA tensor."""
+    t = _torch()
+    if prec not in _lib.PREC_BY_NAME:
+        raise ValueError(f"unknown precision {prec!r}")
+    pid = _lib.PREC_BY_NAME[prec]
+    dt = t.float64 if pid == _lib.PREC_FP64 else t.float32
+    for x, shape, name in ((d, (cfg.N, cfg.C, cfg.H, cfg.W), "d"),
+                           (dy, (cfg.N, cfg.K, cfg.out_h, cfg.out_w), "dy")):
+        if not isinstance(x, t.Tensor) or not x.is_cuda:
+            raise ValueError(f"{name} must be a CUDA tensor")
+        if tuple(x.shape) != shape or x.dtype != dt or not x.is_contiguous():
+            raise ValueError(f"{name}: expected contiguous {dt} {shape}, got {x.dtype} "
+                             f"{tuple(x.shape)}")
+    desc = _lib.LayerDesc(cfg.N, cfg.C, cfg.H, cfg.W, cfg.K, cfg.R, cfg.S, cfg.pad)
+    need = ctypes.c_size_t()
+    _lib.check(_lib.lib.wino_wgrad_workspace(ctypes.byref(desc), pid, int(workspace_limit),
+                                             ctypes.byref(need)), "wino_wgrad_workspace")
+    if workspace is None or workspace.numel() < need.value:
+        workspace = t.empty(need.value, dtype=t.uint8, device=d.device)
+    dg = t.empty((cfg.K, cfg.C, cfg.R, cfg.S), dtype=dt, device=d.device)
+    _lib.check(_lib.lib.wino_grad_weights(ctypes.byref(desc), pid, d.data_ptr(), dy.data_ptr(),
+                                          dg.data_ptr(), workspace.data_ptr(),
+                                          workspace.numel(), int(workspace_limit),
+                                          _stream_handle(stream)), "wino_grad_weights")
+    return dg
+
+
+def winograd_grad_weights(d, dy, cfg: LayerConfig, alg_w: Optional[WinogradAlgorithm] = None,
+                          counter: Optional[OpCounter] = None, prec: Optional[str] = None) -> Tensor4:
+    """dL/dFilter via F(3x3, 2x2) on the GPU (engine.py:278-328): same
+    validation and exceptions, counter ``"mul" += 16*K*B*C`` (the reference's
+    batched_matmul over the tile axis), fresh read-only output."""
+    if alg_w is None:
+        if cfg.R != 3 or cfg.S != 3:
+            raise ValueError(f"default weight-gradient algorithm needs R=S=3, "
+                             f"got {cfg.R}x{cfg.S}")
+        alg_w = builtin(3, 2)
+    if alg_w.m != cfg.R or cfg.R != cfg.S:
+        raise ValueError(f"algorithm F({alg_w.m},{alg_w.r}) cannot produce "
+                         f"{cfg.R}x{cfg.S} gradients")
+    if (alg_w.m, alg_w.r) != (3, 2):
+        raise ValueError(f"GPU path implements F(3,2) for weight gradients, not {alg_w.label}")
+    dp, yp = precision_of(d), precision_of(dy)
+    if dp != yp:
+        raise ValueError(f"mixed precisions: {dp} vs {yp}")
+    if tuple(d.shape) != (cfg.N, cfg.C, cfg.H, cfg.W):
+        raise ValueError(f"data shape {d.shape} does not match {cfg}")
+    if tuple(dy.shape) != (cfg.N, cfg.K, cfg.out_h, cfg.out_w):
+        raise ValueError(f"dY shape {dy.shape} does not match {cfg}")
+    prec = prec or default_prec(dp)
+    if (prec == "fp64") != (dp is Precision.FP64):
+        raise ValueError(f"prec {prec!r} does not match data precision {dp.value}")
+    t = _torch()
+    d_dev = t.from_numpy(np.array(d.data, order="C")).to("cuda")
+    y_dev = t.from_numpy(np.array(dy.data, order="C")).to("cuda")
+    dg = grad_weights_device(d_dev, y_dev, cfg, prec)
+    if counter is not None:
+        B = cfg.N * (-(-cfg.out_h // 2)) * (-(-cfg.out_w // 2))
+        counter.add("mul", 16 * cfg.K * B * cfg.C)
+    return Tensor4._wrap(dg.cpu().numpy(), _out_precision(dp))

@@ -53,6 +53,10 @@ _EXACT = {
     (2, 3): (((1, 0, -1, 0), (0, 1, 1, 0), (0, -1, 1, 0), (0, 1, 0, -1)),
              ((1, 0, 0), (_F(1, 2), _F(1, 2), _F(1, 2)), (_F(1, 2), _F(-1, 2), _F(1, 2)), (0, 0, 1)),
              ((1, 1, 1, 0), (0, 1, -1, -1))),
+    # F(3,2): the weight-gradient algorithm F(3x3, 2x2) (winograd.py:171-189)
+    (3, 2): (((1, 0, -1, 0), (0, 1, 1, 0), (0, -1, 1, 0), (0, -1, 0, 1)),
+             ((1, 0), (_F(1, 2), _F(1, 2)), (_F(1, 2), _F(-1, 2)), (0, 1)),
+             ((1, 1, 1, 0), (0, 1, -1, 0), (0, 1, 1, 1))),
     (4, 3): (((4, 0, -5, 0, 1, 0), (0, -4, -4, 1, 1, 0), (0, 4, -4, -1, 1, 0),
               (0, -2, -1, 2, 1, 0), (0, 2, -1, -2, 1, 0), (0, 4, 0, -5, 0, 1)),
              ((_F(1, 4), 0, 0), (_F(-1, 6), _F(-1, 6), _F(-1, 6)), (_F(-1, 6), _F(1, 6), _F(-1, 6)),
@@ -96,7 +100,8 @@ class WinogradAlgorithm:
 
 
 def builtin(m: int, r: int) -> WinogradAlgorithm:
-    """Builtin F(m, r) on the GPU path: (2,3) and (4,3) (winograd.py:225-232)."""
+    """Builtin F(m, r) (winograd.py:225-232): (2,3) and (4,3) for the forward,
+    (3,2) for the weight gradient."""
     try:
         bt, g, at = _EXACT[(m, r)]
     except KeyError:
@@ -104,7 +109,7 @@ def builtin(m: int, r: int) -> WinogradAlgorithm:
                        f"{sorted(_EXACT)}") from None
     conv = lambda rows: tuple(tuple(Fraction(v) for v in row) for row in rows)
     return WinogradAlgorithm(m=m, r=r, BT=conv(bt), G=conv(g), AT=conv(at),
-                             flops_1d=_FLOPS_1D[(m, r)], name=f"F({m},{r})")
+                             flops_1d=_FLOPS_1D.get((m, r)), name=f"F({m},{r})")
 
 
 def builtin_sizes():
