@@ -616,8 +616,29 @@ __device__ __forceinline__ float load_op(const void* U, size_t idx, size_t plane
   }
 }
 
+// CP contiguous values (16-byte aligned) as vector shared-memory loads.
+template <typename T, int CP>
+__device__ __forceinline__ void load_vec(const T* p, T (&v)[CP]) {
+  if constexpr (sizeof(T) == 4 && CP % 4 == 0) {
+#pragma unroll
+    for (int q = 0; q < CP / 4; ++q) {
+      const float4 x = reinterpret_cast<const float4*>(p)[q];
+      v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
+    }
+  } else if constexpr (sizeof(T) == 4 && CP == 2) {
+    const float2 x = *reinterpret_cast<const float2*>(p);
+    v[0] = x.x; v[1] = x.y;
+  } else {
+#pragma unroll
+    for (int q = 0; q < CP / 2; ++q) {
+      const double2 x = reinterpret_cast<const double2*>(p)[q];
+      v[2 * q] = x.x; v[2 * q + 1] = x.y;
+    }
+  }
+}
+
 template <int M, int PREC, int CP>
-__global__ void __launch_bounds__(256) fused_smallc_kernel(
+__global__ void __launch_bounds__(256, 2) fused_smallc_kernel(
     const typename OpStore<PREC>::T* __restrict__ d, const void* __restrict__ U,
     typename OpStore<PREC>::T* __restrict__ y, int C, int H, int W, int K, int pad, int th,
     int tw, int oh, int ow, int c_pad) {
@@ -663,7 +684,7 @@ __global__ void __launch_bounds__(256) fused_smallc_kernel(
 #pragma unroll
     for (int xi = 0; xi < AL; ++xi)
 #pragma unroll
-      for (int nu = 0; nu < AL; ++nu) s_v[((xi * AL + nu) * CP + c) * 32 + lane] = out[xi][nu];
+      for (int nu = 0; nu < AL; ++nu) s_v[((xi * AL + nu) * 32 + lane) * CP + c] = out[xi][nu];
   }
   const int t = tx0 + lane;
   const size_t plane = static_cast<size_t>(A2) * K * c_pad;
@@ -685,24 +706,56 @@ __global__ void __launch_bounds__(256) fused_smallc_kernel(
     }
     __syncthreads();
     if (t >= tw) continue;
-    for (int kk = warp; kk < kn; kk += 8) {
-      T mm[AL][AL];
-      const T* urow = s_u + kk * CP;
+    // Warp = 4 filters x 32 tiles (lane = tile).  Per component: one vector
+    // load of the tile's CP transformed channels, one broadcast vector load
+    // of each filter's CP transformed weights, 4*CP FMAs.  The inverse
+    // transform is folded per transform row xi, so only the 4 output tiles
+    // and one row of M stay live:  Z[j] = sum_nu AT[j][nu] M[xi][nu],
+    // Y[i][j] += AT[i][xi] Z[j].
+    static_assert(kSmallKB == 4 * 8, "8 warps x 4 filters per chunk");
+    const int k0 = warp * 4;
+    T out[4][M][M] = {};
 #pragma unroll
-      for (int comp = 0; comp < A2; ++comp) {
-        const T* uc = urow + comp * kSmallKB * CP;
-        const T* vc = s_v + comp * CP * 32 + lane;
-        T acc = uc[0] * vc[0];
+    for (int xi = 0; xi < AL; ++xi) {
+      T mrow[4][AL];
 #pragma unroll
-        for (int c = 1; c < CP; ++c) acc = fma(uc[c], vc[c * 32], acc);
-        mm[comp / AL][comp % AL] = acc;
+      for (int nu = 0; nu < AL; ++nu) {
+        const int comp = xi * AL + nu;
+        T v[CP];
+        load_vec<T, CP>(s_v + (comp * 32 + lane) * CP, v);
+#pragma unroll
+        for (int f = 0; f < 4; ++f) {
+          T u[CP];
+          load_vec<T, CP>(s_u + (comp * kSmallKB + k0 + f) * CP, u);
+          T acc = u[0] * v[0];
+#pragma unroll
+          for (int c = 1; c < CP; ++c) acc = fma(u[c], v[c], acc);
+          mrow[f][nu] = acc;
+        }
       }
-      T out[M][M];
-      sandwich<T, M, AL>(mm, out, [](int i, int j) { return A::AT(i, j); });
-      const int k = kc + kk;
-      const int vr = min(M, oh - M * ty), vc = min(M, ow - M * t);
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+          T z = T(0);
+          bool first = true;
+#pragma unroll
+          for (int nu = 0; nu < AL; ++nu) {
+            const double cf = A::AT(j, nu);
+            z = mac(z, cf, mrow[f][nu], first);
+            if (cf != 0.0) first = false;
+          }
+#pragma unroll
+          for (int i = 0; i < M; ++i) out[f][i][j] = mac(out[f][i][j], A::AT(i, xi), z, false);
+        }
+    }
+    const int vr = min(M, oh - M * ty), vc = min(M, ow - M * t);
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      const int k = kc + k0 + f;
+      if (k0 + f >= kn) break;
       T* dst = y + ((static_cast<size_t>(n) * K + k) * oh + M * ty) * ow + M * t;
-      store_tile<M>(dst, ow, vr, vc, out);
+      store_tile<M>(dst, ow, vr, vc, out[f]);
     }
   }
 }
