@@ -235,6 +235,22 @@ __device__ __forceinline__ uint32_t swz_chunk(uint32_t r, uint32_t j) {
   else return j ^ ((r >> 2) & 1u);
 }
 
+// 3xTF32 split of one 16-byte chunk of fp32 operand in shared memory:
+// hi = rna_tf32(x) written back in place, lo = x - hi (exact) to `lo`.
+// The split is element-wise, so it is layout-agnostic (any swizzle).
+__device__ __forceinline__ void split_tf32_chunk(float4* hi, float4* lo) {
+  float4 x = *hi;
+  float4 h, l;
+  uint32_t b;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(x.x)); h.x = __uint_as_float(b);
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(x.y)); h.y = __uint_as_float(b);
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(x.z)); h.z = __uint_as_float(b);
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(x.w)); h.w = __uint_as_float(b);
+  l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
+  *hi = h;
+  *lo = l;
+}
+
 // ---------------------------------------------------------------- clusters
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;

@@ -70,7 +70,7 @@ struct FCfg {
   static constexpr int xbytes = alpha * fo * fls * 4;  // Z receive buffer (aliases the ring)
   static constexpr int ring = stages * stage_bytes;
   static constexpr int bar_off = ring > xbytes ? ring : xbytes;
-  static constexpr int smem = bar_off + 256 + 1024;
+  static constexpr int smem = bar_off + 512 + 1024;
   static constexpr int tmem_cols = 512;
   static constexpr int TT = 8;                     // tiles per TMEM load in the epilogue
   static_assert(alpha * Pb <= tmem_cols, "accumulators exceed TMEM");
@@ -223,10 +223,23 @@ __device__ __forceinline__ void v_row(const float* __restrict__ src, int W, cons
 // channel chunk j): it forms V[S][nu] for cpc channels and stores one 16-byte
 // chunk per nu.  The loads and arithmetic of a stage run before the wait for
 // the ring slot, so they overlap the MMAs still reading it.
+// 3xTF32 keeps one fp32 plane of U (and of a staged V) in HBM: once the TMA
+// bytes of the stage have landed (tmaf), the transform warps split them into
+// hi = rna_tf32(x) in place and lo = x - hi before releasing the stage.
+template <int PREC>
+__device__ __forceinline__ void split_stage(unsigned char* base, int bytes_hi, int tid,
+                                            int nthreads) {
+  if constexpr (PREC == kFP32) {
+    float4* hi = reinterpret_cast<float4*>(base);
+    float4* lo = reinterpret_cast<float4*>(base + bytes_hi);
+    for (int i = tid; i < bytes_hi / 16; i += nthreads) ptx::split_tf32_chunk(hi + i, lo + i);
+  }
+}
+
 template <int M, int PREC, int S, bool VEC>
 __device__ __forceinline__ void transform_loop_v(const FusedParams& a, unsigned char* smem,
-                                                 uint64_t* full, uint64_t* empty, int tid, int pb,
-                                                 int kb0, int kb1) {
+                                                 uint64_t* full, uint64_t* empty, uint64_t* tmaf,
+                                                 int tid, int pb, int kb0, int kb1) {
   using Cf = FCfg<M, PREC>;
   constexpr int AL = Cf::alpha, Pb = Cf::Pb, CPC = Cf::cpc, NG = Cf::NT / Pb;
   const int t = tid % Pb, jg = tid / Pb;
@@ -283,6 +296,10 @@ __device__ __forceinline__ void transform_loop_v(const FusedParams& a, unsigned 
     }
     // idle threads must also see the slot free before their warp re-arms it
     if (!waited) ptx::mbar_wait(&empty[st], ((it / Cf::stages) & 1) ^ 1);
+    if constexpr (PREC == kFP32) {
+      ptx::mbar_wait(&tmaf[st], (it / Cf::stages) & 1);
+      split_stage<PREC>(smem + st * Cf::stage_bytes, Cf::alpha * Cf::u_slot, tid, Cf::NT);
+    }
     ptx::fence_async_smem();
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive(&full[st]);
@@ -291,27 +308,27 @@ __device__ __forceinline__ void transform_loop_v(const FusedParams& a, unsigned 
 
 template <int M, int PREC, int S>
 __device__ __forceinline__ void transform_loop(const FusedParams& a, unsigned char* smem,
-                                               uint64_t* full, uint64_t* empty, int tid, int pb,
-                                               int kb0, int kb1) {
+                                               uint64_t* full, uint64_t* empty, uint64_t* tmaf,
+                                               int tid, int pb, int kb0, int kb1) {
   if (a.vec)
-    transform_loop_v<M, PREC, S, true>(a, smem, full, empty, tid, pb, kb0, kb1);
+    transform_loop_v<M, PREC, S, true>(a, smem, full, empty, tmaf, tid, pb, kb0, kb1);
   else
-    transform_loop_v<M, PREC, S, false>(a, smem, full, empty, tid, pb, kb0, kb1);
+    transform_loop_v<M, PREC, S, false>(a, smem, full, empty, tmaf, tid, pb, kb0, kb1);
 }
 
 template <int M, int PREC>
 __device__ __forceinline__ void transform_dispatch(int s, const FusedParams& a, unsigned char* smem,
-                                                   uint64_t* full, uint64_t* empty, int tid, int pb,
-                                                   int kb0, int kb1) {
+                                                   uint64_t* full, uint64_t* empty, uint64_t* tmaf,
+                                                   int tid, int pb, int kb0, int kb1) {
   switch (s) {
-    case 0: transform_loop<M, PREC, 0>(a, smem, full, empty, tid, pb, kb0, kb1); break;
-    case 1: transform_loop<M, PREC, 1>(a, smem, full, empty, tid, pb, kb0, kb1); break;
-    case 2: transform_loop<M, PREC, 2>(a, smem, full, empty, tid, pb, kb0, kb1); break;
-    case 3: transform_loop<M, PREC, 3>(a, smem, full, empty, tid, pb, kb0, kb1); break;
+    case 0: transform_loop<M, PREC, 0>(a, smem, full, empty, tmaf, tid, pb, kb0, kb1); break;
+    case 1: transform_loop<M, PREC, 1>(a, smem, full, empty, tmaf, tid, pb, kb0, kb1); break;
+    case 2: transform_loop<M, PREC, 2>(a, smem, full, empty, tmaf, tid, pb, kb0, kb1); break;
+    case 3: transform_loop<M, PREC, 3>(a, smem, full, empty, tmaf, tid, pb, kb0, kb1); break;
     default:
       if constexpr (M == 4) {
-        if (s == 4) transform_loop<M, PREC, 4>(a, smem, full, empty, tid, pb, kb0, kb1);
-        else transform_loop<M, PREC, 5>(a, smem, full, empty, tid, pb, kb0, kb1);
+        if (s == 4) transform_loop<M, PREC, 4>(a, smem, full, empty, tmaf, tid, pb, kb0, kb1);
+        else transform_loop<M, PREC, 5>(a, smem, full, empty, tmaf, tid, pb, kb0, kb1);
       }
       break;
   }
@@ -336,7 +353,9 @@ __global__ void __launch_bounds__(FCfg<M, PREC>::threads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cf::bar_off);
   uint64_t* empty = full + STAGES;
   uint64_t* accf = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+  uint64_t* tmaf = accf + 1;  // [STAGES] 3xTF32: TMA bytes landed (split pending)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmaf + STAGES);
+  constexpr bool SPLIT = (PREC == kFP32);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -351,8 +370,10 @@ __global__ void __launch_bounds__(FCfg<M, PREC>::threads, 1)
     if constexpr (VT) ptx::prefetch_tmap(&tmV);
     for (int i = 0; i < STAGES; ++i) {
       // TMA expect_tx (+ one arrive per transform warp when V is formed in-kernel)
-      ptx::mbar_init(&full[i], VT ? 1 : 1 + Cf::NT / 32);
+      // 3xTF32: one arrive per transform warp once the hi/lo split is done
+      ptx::mbar_init(&full[i], SPLIT ? Cf::NT / 32 : (VT ? 1 : 1 + Cf::NT / 32));
       ptx::mbar_init(&empty[i], 1);
+      ptx::mbar_init(&tmaf[i], 1);
     }
     ptx::mbar_init(accf, 1);
     ptx::fence_mbar_init();
@@ -373,20 +394,18 @@ __global__ void __launch_bounds__(FCfg<M, PREC>::threads, 1)
         const int st = it % STAGES;
         ptx::mbar_wait(&empty[st], ((it / STAGES) & 1) ^ 1);
         unsigned char* ust = smem + st * Cf::stage_bytes;
-        ptx::mbar_arrive_expect_tx(&full[st], VT ? Cf::stage_bytes : Cf::u_bytes);
+        // HBM holds one operand plane (3xTF32 lo planes are made on chip)
+        uint64_t* tb = SPLIT ? &tmaf[st] : &full[st];
+        ptx::mbar_arrive_expect_tx(tb, AL * (Cf::u_slot + (VT ? Cf::v_slot : 0)));
 #pragma unroll
-        for (int h = 0; h < Cf::nsplit; ++h)
-#pragma unroll
-          for (int nu = 0; nu < AL; ++nu)
-            ptx::tma_load_3d(ust + (h * AL + nu) * Cf::u_slot, &tmU, &full[st], kb * Cf::bkc,
-                             kblk * Cf::Kb, h * Cf::a2 + s * AL + nu);
+        for (int nu = 0; nu < AL; ++nu)
+          ptx::tma_load_3d(ust + nu * Cf::u_slot, &tmU, tb, kb * Cf::bkc, kblk * Cf::Kb,
+                           s * AL + nu);
         if constexpr (VT) {
 #pragma unroll
-          for (int h = 0; h < Cf::nsplit; ++h)
-#pragma unroll
-            for (int nu = 0; nu < AL; ++nu)
-              ptx::tma_load_3d(ust + Cf::u_bytes + (h * AL + nu) * Cf::v_slot, &tmV, &full[st],
-                               kb * Cf::bkc, pb * Pb, h * Cf::a2 + s * AL + nu);
+          for (int nu = 0; nu < AL; ++nu)
+            ptx::tma_load_3d(ust + Cf::u_bytes + nu * Cf::v_slot, &tmV, tb, kb * Cf::bkc, pb * Pb,
+                             s * AL + nu);
         }
       }
     }
@@ -434,8 +453,22 @@ __global__ void __launch_bounds__(FCfg<M, PREC>::threads, 1)
     __syncwarp();
   } else {
     // ---------------------------------------------------------- transform
-    if constexpr (!VT)
-      transform_dispatch<M, PREC>(s, a, smem, full, empty, threadIdx.x - 64, pb, kb0, kb1);
+    if constexpr (!VT) {
+      transform_dispatch<M, PREC>(s, a, smem, full, empty, tmaf, threadIdx.x - 64, pb, kb0, kb1);
+    } else if constexpr (SPLIT) {  // staged V and U: only the on-chip hi/lo split
+      const int tid = threadIdx.x - 64;
+      int it = 0;
+      for (int kb = kb0; kb < kb1; ++kb, ++it) {
+        const int st = it % STAGES;
+        ptx::mbar_wait(&tmaf[st], (it / STAGES) & 1);
+        unsigned char* base = smem + st * Cf::stage_bytes;
+        split_stage<PREC>(base, AL * Cf::u_slot, tid, Cf::NT);
+        split_stage<PREC>(base + Cf::u_bytes, AL * Cf::v_slot, tid, Cf::NT);
+        ptx::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&full[st]);
+      }
+    }
   }
 
   // ============================================================ epilogue
@@ -597,7 +630,7 @@ static cudaError_t launch_fused_t(const FusedArgs& f, cudaStream_t s) {
   using Cf = FCfg<M, PREC>;
   alignas(64) CUtensorMap tmU, tmV;
   const uint64_t es = Cf::esize;
-  const uint64_t planes = static_cast<uint64_t>(Cf::nsplit) * Cf::a2;
+  const uint64_t planes = static_cast<uint64_t>(op_splits(PREC)) * Cf::a2;  // planes in HBM
   if (!encode_tmap_3d_sw(&tmU, PREC, f.U, f.C, f.K, planes, f.c_pad * es,
                          static_cast<uint64_t>(f.K) * f.c_pad * es, Cf::bkc, Cf::Kb, Cf::swz))
     return cudaErrorInvalidValue;

@@ -28,7 +28,9 @@
 
 namespace wino {
 
-constexpr int kGemmThreads = 192;  // 6 warps
+// 6 warps (+4 tf32-split warps for 3xTF32)
+template <int PREC>
+constexpr int gemm_threads() { return PREC == kFP32 ? 320 : 192; }
 constexpr int kTileP = 128;        // UMMA M (tiles per CTA)
 
 template <int PREC>
@@ -37,7 +39,7 @@ struct GemmTraits {
   static constexpr int esize = kind ? 4 : 2;
   static constexpr int bk = 128 / esize;     // channels per stage (one 128 B swizzle row)
   static constexpr int uk = 32 / esize;      // channels per tcgen05.mma
-  static constexpr int nsplit = (PREC == kFP32) ? 2 : 1;
+  static constexpr int nsplit = (PREC == kFP32) ? 2 : 1;  // smem planes (HBM holds one)
   static constexpr uint32_t fmt = (PREC == kBF16) ? 1u : (PREC == kFP16 ? 0u : 2u);
 };
 
@@ -51,11 +53,11 @@ struct GemmSmem {
   static constexpr int b_bytes = BN * 128;
   static constexpr int stage_bytes = Tr::nsplit * (a_bytes + b_bytes);
   static constexpr int epi_bytes = kEpiWarps * 2 * kEpiBuf;  // double-buffered per warp
-  static constexpr int avail = 227 * 1024 - 1024 - 256 - epi_bytes;
+  static constexpr int avail = 227 * 1024 - 1024 - 512 - epi_bytes;
   static constexpr int stages = avail / stage_bytes >= 6 ? 6 : avail / stage_bytes;
   static constexpr int epi_offset = stages * stage_bytes;
   static constexpr int bar_offset = epi_offset + epi_bytes;
-  static constexpr int total = bar_offset + 256 + 1024;  // barriers + alignment slack
+  static constexpr int total = bar_offset + 512 + 1024;  // barriers + alignment slack
 };
 
 // Persistent, warp-specialised tcgen05 GEMM.  Work unit = (split, comp,
@@ -64,7 +66,7 @@ struct GemmSmem {
 // the MMAs of unit j+1.  Split-C units (small-P layers) write partial sums to
 // separate M slices that the output transform adds in a fixed order.
 template <int PREC, int BN>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
     wgemm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmU,
                     const __grid_constant__ CUtensorMap tmM, int a2, int num_kb,
                     int kb_per_split, int n_pblk, int n_kblk, int n_units) {
@@ -81,7 +83,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;   // [2] accumulator ready
   uint64_t* tempty = tfull + 2;       // [2] accumulator drained
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* sfull = tempty + 2;       // [STAGES] 3xTF32: hi/lo split of the stage done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sfull + STAGES);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -98,6 +101,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       ptx::mbar_init(&tfull[b], 1);
       ptx::mbar_init(&tempty[b], 128);
     }
+    for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&sfull[s], 4);  // one arrive per split warp
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc(tmem_slot, 2 * BN);
@@ -131,14 +135,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const int s = it % STAGES;
           ptx::mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
           unsigned char* st = smem + s * Sm::stage_bytes;
-          ptx::mbar_arrive_expect_tx(&full[s], Sm::stage_bytes);
-#pragma unroll
-          for (int h = 0; h < Tr::nsplit; ++h) {
-            ptx::tma_load_3d(st + h * Sm::a_bytes, &tmV, &full[s], kb * Tr::bk, pb * kTileP,
-                             comp + h * a2);
-            ptx::tma_load_3d(st + Tr::nsplit * Sm::a_bytes + h * Sm::b_bytes, &tmU, &full[s],
-                             kb * Tr::bk, kbk * BN, comp + h * a2);
-          }
+          // HBM holds one plane; 3xTF32's lo planes are produced on chip
+          ptx::mbar_arrive_expect_tx(&full[s], Sm::a_bytes + Sm::b_bytes);
+          ptx::tma_load_3d(st, &tmV, &full[s], kb * Tr::bk, pb * kTileP, comp);
+          ptx::tma_load_3d(st + Tr::nsplit * Sm::a_bytes, &tmU, &full[s], kb * Tr::bk, kbk * BN,
+                           comp);
         }
       }
     }
@@ -158,7 +159,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
-          ptx::mbar_wait(&full[s], (it / STAGES) & 1);
+          if constexpr (Tr::nsplit == 2)
+            ptx::mbar_wait(&sfull[s], (it / STAGES) & 1);
+          else
+            ptx::mbar_wait(&full[s], (it / STAGES) & 1);
           ptx::tc_fence_after();
           const uint32_t st = ptx::smem_u32(smem + s * Sm::stage_bytes);
           const uint32_t a_hi = st, a_lo = st + Sm::a_bytes;
@@ -183,6 +187,36 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           ptx::umma_commit(&empty[s]);  // frees the smem slot when these MMAs retire
         }
         ptx::umma_commit(&tfull[acc]);  // accumulator complete
+      }
+    }
+  } else if (warp >= 6) {
+    // ------------------------------------------------------------ 3xTF32 split
+    // (warps 6-9 exist only for PREC == kFP32) hi = rna_tf32(x) in place,
+    // lo = x - hi into the stage's lo planes, then release the stage to MMA.
+    if constexpr (Tr::nsplit == 2) {
+      const int tid = threadIdx.x - 192;
+      int it = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        int pb, kbk, comp, split;
+        decode(u, pb, kbk, comp, split);
+        const int kb0 = split * kb_per_split;
+        const int kb1 = min(num_kb, kb0 + kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % STAGES;
+          ptx::mbar_wait(&full[s], (it / STAGES) & 1);
+          unsigned char* st = smem + s * Sm::stage_bytes;
+          float4* ahi = reinterpret_cast<float4*>(st);
+          float4* alo = reinterpret_cast<float4*>(st + Sm::a_bytes);
+          float4* bhi = reinterpret_cast<float4*>(st + 2 * Sm::a_bytes);
+          float4* blo = reinterpret_cast<float4*>(st + 2 * Sm::a_bytes + Sm::b_bytes);
+#pragma unroll 4
+          for (int i = tid; i < Sm::a_bytes / 16; i += 128) ptx::split_tf32_chunk(ahi + i, alo + i);
+#pragma unroll 4
+          for (int i = tid; i < Sm::b_bytes / 16; i += 128) ptx::split_tf32_chunk(bhi + i, blo + i);
+          ptx::fence_async_smem();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&sfull[s]);
+        }
       }
     }
   } else {
@@ -305,7 +339,7 @@ static cudaError_t launch_tc(const GemmArgs& a, cudaStream_t s) {
   using Sm = GemmSmem<PREC, BN>;
   alignas(64) CUtensorMap tmV, tmU;
   const uint64_t es = Tr::esize;
-  const uint64_t planes = static_cast<uint64_t>(Tr::nsplit) * a.a2;
+  const uint64_t planes = static_cast<uint64_t>(op_splits(PREC)) * a.a2;  // planes in HBM
   if (!encode_tmap_3d(&tmV, PREC, a.V, a.C, a.Pc, planes, a.c_pad * es, a.Pc * a.c_pad * es,
                       Tr::bk, kTileP))
     return cudaErrorInvalidValue;
@@ -334,7 +368,7 @@ static cudaError_t launch_tc(const GemmArgs& a, cudaStream_t s) {
   const long long units = static_cast<long long>(n_pblk) * n_kblk * a.a2 * splits;
   if (units > 0x7fffffffLL) return cudaErrorInvalidValue;
   const int grid = static_cast<int>(units < num_sms() ? units : num_sms());
-  launch_k(kern, dim3(grid), dim3(kGemmThreads), Sm::total, s, tmV, tmU, tmM, a.a2, num_kb, kbps,
+  launch_k(kern, dim3(grid), dim3(gemm_threads<PREC>()), Sm::total, s, tmV, tmU, tmM, a.a2, num_kb, kbps,
            n_pblk, n_kblk, static_cast<int>(units));
   return cudaGetLastError();
 }

@@ -27,7 +27,10 @@ inline int op_bytes(int prec) {
     default: return 4;
   }
 }
-inline int op_splits(int prec) { return prec == kFP32 ? 2 : 1; }
+// Operand planes in HBM.  3xTF32 keeps ONE fp32 plane in memory; the GEMM
+// kernels split each landed shared-memory stage into hi = rna_tf32(x) and
+// lo = x - hi on chip, so U and V cost 4 bytes per element, not 8.
+inline int op_splits(int) { return 1; }
 
 // ---- launchers (defined in wino_transforms.cu / wino_gemm.cu) -------------
 // All return cudaError_t of the launch.

@@ -20,15 +20,10 @@ template <int PREC>
 struct OpStore;
 
 template <>
-struct OpStore<kFP32> {  // 3xTF32: hi = rna_tf32(x), lo = x - hi (exact in fp32)
+struct OpStore<kFP32> {  // 3xTF32: plain fp32 in memory; the GEMM splits hi/lo on chip
   using T = float;
-  __device__ static void put(void* base, size_t idx, size_t plane, float x) {
-    uint32_t hi_bits;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi_bits) : "f"(x));
-    const float hi = __uint_as_float(hi_bits);
-    float* p = static_cast<float*>(base);
-    p[idx] = hi;
-    p[idx + plane] = x - hi;
+  __device__ static void put(void* base, size_t idx, size_t, float x) {
+    static_cast<float*>(base)[idx] = x;
   }
 };
 template <>
@@ -604,10 +599,7 @@ constexpr int kSmallKB = 32;
 
 template <int PREC>
 __device__ __forceinline__ float load_op(const void* U, size_t idx, size_t plane) {
-  if constexpr (PREC == kFP32) {
-    const float* u = static_cast<const float*>(U);
-    return u[idx] + u[idx + plane];  // hi + lo = the exact fp32 transform
-  } else if constexpr (PREC == kTF32) {
+  if constexpr (PREC == kFP32 || PREC == kTF32) {  // fp32 (3xTF32) / tf32-rounded plane
     return static_cast<const float*>(U)[idx];
   } else if constexpr (PREC == kBF16) {
     return __bfloat162float(static_cast<const __nv_bfloat16*>(U)[idx]);
