@@ -120,6 +120,30 @@ bool encode_tmap_3d_sw(void* map_out, int prec, const void* base, uint64_t d0, u
   return true;
 }
 
+// fp32 3D map with a 3D box (no swizzle, zero OOB fill): the output transform's
+// M[comp][k][p] staging box.
+bool encode_tmap_3d_box(void* map_out, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                        uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box0,
+                        uint32_t box1, uint32_t box2) {
+  if (!load_encode()) {
+    set_error("cuTensorMapEncodeTiled unavailable (driver too old?)");
+    return false;
+  }
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
+  cuuint32_t box[3] = {box0, box1, box2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(reinterpret_cast<CUtensorMap*>(map_out), CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                        3, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (3d box) failed (%d)", (int)r);
+    return false;
+  }
+  return true;
+}
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* v = getenv("WINO_NO_PDL");

@@ -143,6 +143,9 @@ bool encode_tmap_nchw_f32(void* map_out, const void* base, int N, int C, int H, 
 bool encode_tmap_3d_sw(void* map_out, int prec, const void* base, uint64_t d0, uint64_t d1,
                        uint64_t d2, uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box0,
                        uint32_t box1, int swizzle_bytes);
+bool encode_tmap_3d_box(void* map_out, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                        uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box0,
+                        uint32_t box1, uint32_t box2);
 bool encode_tmap_3d(void* map_out, int prec, const void* base, uint64_t d0, uint64_t d1,
                     uint64_t d2, uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box0,
                     uint32_t box1);

@@ -293,6 +293,69 @@ __global__ void __launch_bounds__(128, 8) output_transform_kernel(const TA* __re
   store_tile<M>(dst, ow, vr, vc, out);
 }
 
+// TMA-staged variant (fp32, no split-C): one 3D TMA box brings a block's
+// M[comp][k0..k0+OF)[p0..p0+128) (alpha^2 x OF x 128 fp32) into shared memory
+// -- all of the block's loads in flight at once without any register cost --
+// then thread = tile forms A^T M A for each of the OF filters from smem
+// (lane-contiguous, conflict-free) and stores the clipped tiles.
+constexpr int kOutTP = 128;  // tiles per block
+template <int M>
+struct OutTma {
+  static constexpr int alpha = M + 2;
+  static constexpr int OF = (M == 4) ? 2 : 4;  // filters per block
+  static constexpr int bytes = alpha * alpha * OF * kOutTP * 4;
+};
+
+template <int M>
+__global__ void __launch_bounds__(kOutTP) output_transform_tma_kernel(
+    const __grid_constant__ CUtensorMap tmM, float* __restrict__ y, int K, int th, int tw, int oh,
+    int ow, int row0, long long Pc) {
+  using A = Alg<M>;
+  using Cfg = OutTma<M>;
+  constexpr int AL = A::alpha;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* s = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
+                                      ~static_cast<uintptr_t>(127));
+  __shared__ uint64_t bar;
+  const int p0 = blockIdx.x * kOutTP;
+  const int k0 = blockIdx.y * Cfg::OF;
+  griddep_launch();
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bar, 1);
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  griddep_wait();
+  if (threadIdx.x == 0) {
+    ptx::mbar_arrive_expect_tx(&bar, Cfg::bytes);
+    ptx::tma_load_3d(s, &tmM, &bar, p0, k0, 0);
+  }
+  ptx::mbar_wait(&bar, 0);
+  const int t = threadIdx.x;
+  const long long p = static_cast<long long>(p0) + t;
+  if (p >= Pc) return;
+  const long long gp = static_cast<long long>(row0) * tw + p;
+  const long long per_img = static_cast<long long>(th) * tw;
+  const int n = static_cast<int>(gp / per_img);
+  const int rest = static_cast<int>(gp - n * per_img);
+  const int ty = rest / tw, tx = rest - ty * tw;
+  const int vr = min(M, oh - M * ty), vc = min(M, ow - M * tx);
+#pragma unroll
+  for (int f = 0; f < Cfg::OF; ++f) {
+    const int k = k0 + f;
+    if (k >= K) break;
+    float in[AL][AL];
+#pragma unroll
+    for (int xi = 0; xi < AL; ++xi)
+#pragma unroll
+      for (int nu = 0; nu < AL; ++nu) in[xi][nu] = s[((xi * AL + nu) * Cfg::OF + f) * kOutTP + t];
+    float out[M][M];
+    sandwich<float, M, AL>(in, out, [](int i, int j) { return A::AT(i, j); });
+    float* dst = y + ((static_cast<size_t>(n) * K + k) * oh + M * ty) * ow + M * tx;
+    store_tile<M>(dst, ow, vr, vc, out);
+  }
+}
+
 // Write an m x m output tile: one vector store per row for full tiles whose
 // rows are vector-aligned (a warp then writes 32 adjacent tiles = whole lines),
 // clipped scalar stores for edge tiles (engine.py:246-253).
@@ -557,10 +620,38 @@ cudaError_t launch_input_transform(int m, int prec, const void* d, void* V, int 
                 : input_dispatch<4>(prec, d, V, N, C, H, W, pad, th, tw, row0, rows, Pc, c_pad, s);
 }
 
+template <int M>
+static cudaError_t output_tma_launch(const void* Mbuf, void* y, int K, int th, int tw, int oh,
+                                     int ow, int row0, long long Pc, long long m_ld,
+                                     cudaStream_t s) {
+  using Cfg = OutTma<M>;
+  alignas(64) CUtensorMap tmM;
+  // M [a2][K][m_ld] fp32, box (128 tiles, OF filters, a2 components), no swizzle
+  if (!encode_tmap_3d_box(&tmM, Mbuf, static_cast<uint64_t>(Pc), static_cast<uint64_t>(K),
+                          static_cast<uint64_t>(Cfg::alpha * Cfg::alpha), m_ld * 4ull,
+                          static_cast<uint64_t>(K) * m_ld * 4ull, kOutTP, Cfg::OF,
+                          Cfg::alpha * Cfg::alpha))
+    return cudaErrorInvalidValue;
+  auto kern = output_transform_tma_kernel<M>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::bytes + 128);
+    max_carveout(kern);
+    configured = true;
+  }
+  const dim3 grid(static_cast<unsigned>((Pc + kOutTP - 1) / kOutTP), (K + Cfg::OF - 1) / Cfg::OF);
+  launch_k(kern, grid, dim3(kOutTP), static_cast<size_t>(Cfg::bytes + 128), s, tmM,
+           static_cast<float*>(y), K, th, tw, oh, ow, row0, Pc);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_output_transform(int m, int prec, const void* Mbuf, void* y, int N, int K,
                                     int th, int tw, int oh, int ow, int row0, long long Pc,
                                     long long m_ld, int splits, cudaStream_t s) {
   if (Pc <= 0 || K <= 0) return cudaSuccess;
+  if (prec != kFP64 && splits == 1 && getenv("WINO_NO_TMA_OUTPUT") == nullptr)
+    return m == 2 ? output_tma_launch<2>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s)
+                  : output_tma_launch<4>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s);
   const dim3 grid(static_cast<unsigned>((Pc + 127) / 128), K);
   static bool configured = false;
   if (!configured) {
