@@ -177,8 +177,7 @@ __device__ __forceinline__ void load_row(const float* __restrict__ row, int u, c
 }
 
 // Row S of B^T d B for one channel: r[x] = sum_u BT[S][u] d[u][x], then
-// V[nu] = sum_x BT[nu][x] r[x] -- the same operation order as the unfused
-// input transform (sandwich(), winograd_mats.cuh), so V is bit-identical.
+// V[nu] = sum_x BT[nu][x] r[x] (for F(4,3) with the shared-subexpression bt6).
 // Rows with BT[S][u] == 0 are never loaded.
 template <int M, int S, bool VEC>
 __device__ __forceinline__ void v_row(const float* __restrict__ src, int W, const TileGeo& g,
@@ -205,17 +204,21 @@ __device__ __forceinline__ void v_row(const float* __restrict__ src, int W, cons
     }
     r[x] = acc;
   }
+  if constexpr (M == 4) {
+    bt6(r, v);  // shared-subexpression F(4,3) column transform (winograd_mats.cuh)
+  } else {
 #pragma unroll
-  for (int nu = 0; nu < AL; ++nu) {
-    float acc = 0.f;
-    bool first = true;
+    for (int nu = 0; nu < AL; ++nu) {
+      float acc = 0.f;
+      bool first = true;
 #pragma unroll
-    for (int x = 0; x < AL; ++x) {
-      const double c = A::BT(nu, x);
-      acc = mac(acc, c, r[x], first);
-      if (c != 0.0) first = false;
+      for (int x = 0; x < AL; ++x) {
+        const double c = A::BT(nu, x);
+        acc = mac(acc, c, r[x], first);
+        if (c != 0.0) first = false;
+      }
+      v[nu] = acc;
     }
-    v[nu] = acc;
   }
 }
 

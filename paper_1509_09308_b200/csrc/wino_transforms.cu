@@ -229,7 +229,10 @@ __global__ void __launch_bounds__(256) input_transform_kernel(
       for (int i = 0; i < AL; ++i)
 #pragma unroll
         for (int j = 0; j < AL; ++j) in[i][j] = src[i * Cfg::xw + j];
-      sandwich<T, AL, AL>(in, out[h], [](int i, int j) { return A::BT(i, j); });
+      if constexpr (M == 4)
+        bt6_2d(in, out[h]);
+      else
+        sandwich<T, AL, AL>(in, out[h], [](int i, int j) { return A::BT(i, j); });
     }
     const long long p = static_cast<long long>(blockIdx.y) * tw + tx0 + t;  // chunk-local tile
     size_t idx = static_cast<size_t>(p) * c_pad + cbase;
@@ -533,7 +536,10 @@ __global__ void __launch_bounds__(256) input_transform_tma_kernel(
         load_patch<M, AL, Cfg::nv, O0>(sc, Cfg::xwb, x - O0, in);
     }
     float out[AL][AL];
-    sandwich<float, AL, AL>(in, out, [](int i, int j) { return A::BT(i, j); });
+    if constexpr (M == 4)
+      bt6_2d(in, out);
+    else
+      sandwich<float, AL, AL>(in, out, [](int i, int j) { return A::BT(i, j); });
     const long long p = static_cast<long long>(blockIdx.y) * tw + tx0 + t;
     size_t idx = static_cast<size_t>(p) * c_pad + c;
 #pragma unroll
@@ -763,7 +769,10 @@ __global__ void __launch_bounds__(256, 2) fused_smallc_kernel(
     for (int i = 0; i < AL; ++i)
 #pragma unroll
       for (int j = 0; j < AL; ++j) in[i][j] = s_in[(c * AL + i) * XW + lane * M + j];
-    sandwich<T, AL, AL>(in, out, [](int i, int j) { return A::BT(i, j); });
+    if constexpr (M == 4)
+      bt6_2d(in, out);
+    else
+      sandwich<T, AL, AL>(in, out, [](int i, int j) { return A::BT(i, j); });
 #pragma unroll
     for (int xi = 0; xi < AL; ++xi)
 #pragma unroll
