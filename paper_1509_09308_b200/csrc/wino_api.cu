@@ -24,6 +24,7 @@ struct wino_plan_s {
   int bn, splits;
   bool smallc;  // whole layer in the fused tiny-C kernel (no V/M staging)
   int path;     // kPathStaged / kPathFused / kPathHybrid (see plan_create)
+  bool overlap; // staged, several chunks: two chunks in flight on two streams
   int fsplits;  // split-C factor of the fused kernel
   size_t ypart_bytes;
   int rows_total, rows_per_chunk, num_chunks;
@@ -187,7 +188,7 @@ static int cuda_fail(cudaError_t e, const char* what) {
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // Default chunk budget: transform-space staging that stays L2-resident.
-constexpr size_t kDefaultWorkspace = 64ull << 20;
+constexpr size_t kDefaultWorkspace = 128ull << 20;
 
 }  // namespace wino
 
@@ -369,6 +370,22 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
                                     align_up(static_cast<size_t>(L.N) * L.K * oh * ow, 4) * 4,
                                 1024);
   }
+  // ---- staged path with several chunks: two chunks in flight (chunk i+1's
+  // input transform runs under chunk i's GEMM and output transform, on a second
+  // stream), each with half the budget so both stay L2-resident.
+  p->overlap = false;
+  if (p->path == kPathStaged && !p->smallc && p->num_chunks > 1) {
+    long long r2 = static_cast<long long>((budget / 2) / (per_row ? per_row : 1));
+    if (r2 < 1) r2 = 1;
+    p->rows_per_chunk = static_cast<int>(r2);
+    p->num_chunks = (p->rows_total + p->rows_per_chunk - 1) / p->rows_per_chunk;
+    p->chunk_tiles = static_cast<long long>(p->rows_per_chunk) * p->tw;
+    p->v_bytes = align_up(static_cast<size_t>(p->nsplit) * p->a2 * p->chunk_tiles * p->c_pad *
+                              p->esize,
+                          1024);
+    p->m_ld = static_cast<long long>(align_up(static_cast<size_t>(p->chunk_tiles), 4));
+    p->overlap = p->num_chunks > 1;
+  }
   p->m_bytes = (p->smallc || p->path != kPathStaged) ? 0
                         : align_up(static_cast<size_t>(p->splits) * p->a2 * L.K * p->m_ld *
                                        p->acc_bytes,
@@ -406,7 +423,8 @@ int wino_plan_get_info(wino_plan_t p, wino_plan_info_t* info) {
   info->num_chunks = p->num_chunks;
   info->chunk_tiles = p->chunk_tiles;
   info->u_bytes = p->u_bytes;
-  info->workspace_bytes = p->u_bytes + p->v_bytes + p->m_bytes + p->ypart_bytes;
+  info->workspace_bytes =
+      p->u_bytes + (p->overlap ? 2 : 1) * (p->v_bytes + p->m_bytes) + p->ypart_bytes;
   info->launches_per_forward =
       p->smallc ? 1
                 : p->path == kPathFused  ? 1 + (p->fsplits > 1)
@@ -498,40 +516,44 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   StageTimer tm(s, timer);
   unsigned char* ws = static_cast<unsigned char*>(workspace);
-  size_t need = p->v_bytes + p->m_bytes + p->ypart_bytes + (U ? 0 : p->u_bytes);
+  size_t need =
+      (p->overlap ? 2 : 1) * (p->v_bytes + p->m_bytes) + p->ypart_bytes + (U ? 0 : p->u_bytes);
   if (workspace_bytes < need) {
     set_error("workspace too small: %zu < %zu bytes", workspace_bytes, need);
     return WINO_EINVAL;
   }
   // non-FX: G g G^T into the workspace.  Unless stage-timed, it runs on the
   // side stream alongside the input transform and is joined before the GEMM.
+  // The side stream also carries every odd row chunk of a staged plan with
+  // `overlap` (double-buffered V/M), joined back at the end.
   SideStream* side = nullptr;
+  bool filt_side = false;
+  const bool may_overlap = !timer && !p->smallc && p->path != kPathFused &&
+                           getenv("WINO_NO_OVERLAP") == nullptr;
+  const bool chunk_overlap = may_overlap && p->overlap && p->path == kPathStaged;
+  if (may_overlap && (!U || chunk_overlap)) {
+    side = side_stream();
+    if (side && (cudaEventRecord(side->fork, s) != cudaSuccess ||
+                 cudaStreamWaitEvent(side->st, side->fork, 0) != cudaSuccess))
+      side = nullptr;
+  }
   if (!U) {
-    cudaStream_t fs = s;
-    if (!timer && !p->smallc && p->path != kPathFused && getenv("WINO_NO_OVERLAP") == nullptr)
-      side = side_stream();
-    if (side) {
-      if (cudaEventRecord(side->fork, s) != cudaSuccess ||
-          cudaStreamWaitEvent(side->st, side->fork, 0) != cudaSuccess)
-        side = nullptr;
-      else
-        fs = side->st;
-    }
-    cudaError_t e = launch_filter_transform(p->m, p->prec, g, ws, p->L.K, p->L.C, p->c_pad, fs);
+    cudaError_t e = launch_filter_transform(p->m, p->prec, g, ws, p->L.K, p->L.C, p->c_pad,
+                                            side ? side->st : s);
     if (e != cudaSuccess) return cuda_fail(e, "filter transform");
     if (side) {
       e = cudaEventRecord(side->join, side->st);
       if (e != cudaSuccess) return cuda_fail(e, "filter transform join");
+      filt_side = true;
     }
     tm.mark(0);
     U = ws;
     ws += p->u_bytes;
   }
   auto join_filters = [&]() -> cudaError_t {
-    if (!side) return cudaSuccess;
-    cudaError_t e = cudaStreamWaitEvent(s, side->join, 0);
-    side = nullptr;
-    return e;
+    if (!filt_side) return cudaSuccess;
+    filt_side = false;
+    return cudaStreamWaitEvent(s, side->join, 0);
   };
   const wino_layer_t& L = p->L;
   if (p->smallc) {
@@ -577,30 +599,42 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
     }
     return WINO_OK;
   }
-  void* V = ws;
-  void* Mb = ws + p->v_bytes;
+  const size_t vm = p->v_bytes + p->m_bytes;
   for (int ch = 0; ch < p->num_chunks; ++ch) {
     const int row0 = ch * p->rows_per_chunk;
     const int rows = (row0 + p->rows_per_chunk <= p->rows_total) ? p->rows_per_chunk
                                                                   : p->rows_total - row0;
     const long long Pc = static_cast<long long>(rows) * p->tw;
+    // odd chunks on the side stream with the second V/M buffer (stream order
+    // serialises chunk i and i+2, which share a buffer; U precedes on `side`)
+    const bool odd = chunk_overlap && side && (ch & 1);
+    cudaStream_t cs = odd ? side->st : s;
+    unsigned char* V = ws + (odd ? vm : 0);
+    unsigned char* Mb = V + p->v_bytes;
     cudaError_t e = launch_input_transform(p->m, p->prec, d, V, L.N, L.C, L.H, L.W, L.pad, p->th,
-                                           p->tw, row0, rows, Pc, p->c_pad, s);
+                                           p->tw, row0, rows, Pc, p->c_pad, cs);
     if (e != cudaSuccess) return cuda_fail(e, "input transform");
     tm.mark(1);
     GemmArgs ga{V, U, Mb, p->a2, L.K, L.C, p->c_pad, Pc, p->bn, p->splits, p->m_ld};
-    e = join_filters();
-    if (e != cudaSuccess) return cuda_fail(e, "filter transform join");
-    e = launch_batched_gemm(p->prec, ga, s);
+    if (!odd) {
+      e = join_filters();
+      if (e != cudaSuccess) return cuda_fail(e, "filter transform join");
+    }
+    e = launch_batched_gemm(p->prec, ga, cs);
     if (e != cudaSuccess) {
       if (g_err.empty()) return cuda_fail(e, "batched gemm");
       return WINO_ECUDA;
     }
     tm.mark(2);
     e = launch_output_transform(p->m, p->prec, Mb, y, L.N, L.K, p->th, p->tw, p->oh, p->ow, row0,
-                                Pc, p->m_ld, p->splits, s);
+                                Pc, p->m_ld, p->splits, cs);
     if (e != cudaSuccess) return cuda_fail(e, "output transform");
     tm.mark(3);
+  }
+  if (side && (chunk_overlap || filt_side)) {  // join the side stream back into `s`
+    cudaError_t e = cudaEventRecord(side->join, side->st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, side->join, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "side stream join");
   }
   return WINO_OK;
 }
