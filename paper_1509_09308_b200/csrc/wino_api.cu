@@ -487,21 +487,32 @@ struct SideStream {
   cudaStream_t st = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
 };
-SideStream* side_stream() {
-  constexpr int kMaxDev = 64;
-  thread_local SideStream ss[kMaxDev];
+// One side stream per (host thread, device, caller stream): callers that
+// pipeline independent forwards on several streams must not be coupled
+// through a shared side stream.
+SideStream* side_stream(cudaStream_t user) {
+  struct Key {
+    int dev;
+    cudaStream_t user;
+  };
+  constexpr int kMax = 64;
+  thread_local Key keys[kMax];
+  thread_local SideStream ss[kMax];
+  thread_local int n = 0;
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return nullptr;
-  SideStream& x = ss[dev];
-  if (!x.st) {
-    if (cudaStreamCreateWithFlags(&x.st, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming) != cudaSuccess) {
-      x.st = nullptr;
-      return nullptr;
-    }
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  for (int i = 0; i < n; ++i)
+    if (keys[i].dev == dev && keys[i].user == user) return &ss[i];
+  if (n == kMax) return nullptr;
+  SideStream& x = ss[n];
+  if (cudaStreamCreateWithFlags(&x.st, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming) != cudaSuccess) {
+    x = SideStream();
+    return nullptr;
   }
-  return &x;
+  keys[n] = Key{dev, user};
+  return &ss[n++];
 }
 }  // namespace
 
@@ -532,7 +543,7 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
                            getenv("WINO_NO_OVERLAP") == nullptr;
   const bool chunk_overlap = may_overlap && p->overlap && p->path == kPathStaged;
   if (may_overlap && (!U || chunk_overlap)) {
-    side = side_stream();
+    side = side_stream(s);
     if (side && (cudaEventRecord(side->fork, s) != cudaSuccess ||
                  cudaStreamWaitEvent(side->st, side->fork, 0) != cudaSuccess))
       side = nullptr;
