@@ -238,17 +238,28 @@ __device__ __forceinline__ uint32_t swz_chunk(uint32_t r, uint32_t j) {
 // 3xTF32 split of one 16-byte chunk of fp32 operand in shared memory:
 // hi = rna_tf32(x) written back in place, lo = x - hi (exact) to `lo`.
 // The split is element-wise, so it is layout-agnostic (any swizzle).
+// Shared-window 32-bit addresses (ld/st.shared), no generic addressing.
+__device__ __forceinline__ void split_tf32_chunk_s(uint32_t hi, uint32_t lo) {
+  float x0, x1, x2, x3;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(x0), "=f"(x1), "=f"(x2), "=f"(x3)
+               : "r"(hi));
+  uint32_t h0, h1, h2, h3;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h0) : "f"(x0));
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h1) : "f"(x1));
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h2) : "f"(x2));
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h3) : "f"(x3));
+  const float l0 = x0 - __uint_as_float(h0), l1 = x1 - __uint_as_float(h1);
+  const float l2 = x2 - __uint_as_float(h2), l3 = x3 - __uint_as_float(h3);
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(hi), "r"(h0), "r"(h1), "r"(h2),
+               "r"(h3)
+               : "memory");
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(lo), "f"(l0), "f"(l1), "f"(l2),
+               "f"(l3)
+               : "memory");
+}
 __device__ __forceinline__ void split_tf32_chunk(float4* hi, float4* lo) {
-  float4 x = *hi;
-  float4 h, l;
-  uint32_t b;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(x.x)); h.x = __uint_as_float(b);
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(x.y)); h.y = __uint_as_float(b);
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(x.z)); h.z = __uint_as_float(b);
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(x.w)); h.w = __uint_as_float(b);
-  l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
-  *hi = h;
-  *lo = l;
+  split_tf32_chunk_s(smem_u32(hi), smem_u32(lo));
 }
 
 // ---------------------------------------------------------------- clusters

@@ -28,9 +28,10 @@
 
 namespace wino {
 
-// 6 warps (+4 tf32-split warps for 3xTF32)
+// 6 warps (+8 tf32-split warps for 3xTF32)
+constexpr int kSplitWarps = 8;
 template <int PREC>
-constexpr int gemm_threads() { return PREC == kFP32 ? 320 : 192; }
+constexpr int gemm_threads() { return PREC == kFP32 ? 192 + 32 * kSplitWarps : 192; }
 constexpr int kTileP = 128;        // UMMA M (tiles per CTA)
 
 template <int PREC>
@@ -101,7 +102,7 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
       ptx::mbar_init(&tfull[b], 1);
       ptx::mbar_init(&tempty[b], 128);
     }
-    for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&sfull[s], 4);  // one arrive per split warp
+    for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&sfull[s], kSplitWarps);  // one per split warp
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc(tmem_slot, 2 * BN);
@@ -191,7 +192,7 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
     }
   } else if (warp >= 6) {
     // ------------------------------------------------------------ 3xTF32 split
-    // (warps 6-9 exist only for PREC == kFP32) hi = rna_tf32(x) in place,
+    // (warps 6.. exist only for PREC == kFP32) hi = rna_tf32(x) in place,
     // lo = x - hi into the stage's lo planes, then release the stage to MMA.
     if constexpr (Tr::nsplit == 2) {
       const int tid = threadIdx.x - 192;
@@ -204,15 +205,15 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
           ptx::mbar_wait(&full[s], (it / STAGES) & 1);
-          unsigned char* st = smem + s * Sm::stage_bytes;
-          float4* ahi = reinterpret_cast<float4*>(st);
-          float4* alo = reinterpret_cast<float4*>(st + Sm::a_bytes);
-          float4* bhi = reinterpret_cast<float4*>(st + 2 * Sm::a_bytes);
-          float4* blo = reinterpret_cast<float4*>(st + 2 * Sm::a_bytes + Sm::b_bytes);
+          const uint32_t st = ptx::smem_u32(smem + s * Sm::stage_bytes);
+          constexpr int NTS = 32 * kSplitWarps;
 #pragma unroll 4
-          for (int i = tid; i < Sm::a_bytes / 16; i += 128) ptx::split_tf32_chunk(ahi + i, alo + i);
+          for (int i = tid; i < Sm::a_bytes / 16; i += NTS)
+            ptx::split_tf32_chunk_s(st + 16 * i, st + Sm::a_bytes + 16 * i);
 #pragma unroll 4
-          for (int i = tid; i < Sm::b_bytes / 16; i += 128) ptx::split_tf32_chunk(bhi + i, blo + i);
+          for (int i = tid; i < Sm::b_bytes / 16; i += NTS)
+            ptx::split_tf32_chunk_s(st + 2 * Sm::a_bytes + 16 * i,
+                                    st + 2 * Sm::a_bytes + Sm::b_bytes + 16 * i);
           ptx::fence_async_smem();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&sfull[s]);
