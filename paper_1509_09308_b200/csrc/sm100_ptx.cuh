@@ -258,6 +258,33 @@ __device__ __forceinline__ void split_tf32_chunk_s(uint32_t hi, uint32_t lo) {
                "f"(l3)
                : "memory");
 }
+// Four chunks per call: all loads issue before any store (the volatile
+// ld/st asm statements keep program order, so batching is explicit).
+__device__ __forceinline__ void split_tf32_chunk4_s(const uint32_t (&hi)[4],
+                                                    const uint32_t (&lo)[4]) {
+  float x[4][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(x[q][0]), "=f"(x[q][1]), "=f"(x[q][2]), "=f"(x[q][3])
+                 : "r"(hi[q]));
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t h[4];
+    float l[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h[e]) : "f"(x[q][e]));
+      l[e] = x[q][e] - __uint_as_float(h[e]);
+    }
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(hi[q]), "r"(h[0]), "r"(h[1]),
+                 "r"(h[2]), "r"(h[3])
+                 : "memory");
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(lo[q]), "f"(l[0]), "f"(l[1]),
+                 "f"(l[2]), "f"(l[3])
+                 : "memory");
+  }
+}
 __device__ __forceinline__ void split_tf32_chunk(float4* hi, float4* lo) {
   split_tf32_chunk_s(smem_u32(hi), smem_u32(lo));
 }

@@ -61,6 +61,22 @@ struct GemmSmem {
   static constexpr int total = bar_offset + 512 + 1024;  // barriers + alignment slack
 };
 
+// 3xTF32 split of `n` 16-byte chunks at shared address `hi` (lo plane `lo_off`
+// bytes further) by the kSplitWarps split warps: batches of four loads in
+// flight per thread, single chunks for the tail.
+__device__ __forceinline__ void split_region(uint32_t hi, int n, int lo_off, int tid) {
+  constexpr int NTS = 32 * kSplitWarps;
+  int base = 0;
+  for (; base + 4 * NTS <= n; base += 4 * NTS) {
+    const int i = base + tid;
+    const uint32_t h[4] = {hi + 16 * i, hi + 16 * (i + NTS), hi + 16 * (i + 2 * NTS),
+                           hi + 16 * (i + 3 * NTS)};
+    const uint32_t l[4] = {h[0] + lo_off, h[1] + lo_off, h[2] + lo_off, h[3] + lo_off};
+    ptx::split_tf32_chunk4_s(h, l);
+  }
+  for (int i = base + tid; i < n; i += NTS) ptx::split_tf32_chunk_s(hi + 16 * i, hi + 16 * i + lo_off);
+}
+
 // Persistent, warp-specialised tcgen05 GEMM.  Work unit = (split, comp,
 // filter block, tile block); CTAs stride through units.  The accumulator is
 // double-buffered in TMEM (2 x BN columns) so the epilogue of unit j overlaps
@@ -206,14 +222,8 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
           const int s = it % STAGES;
           ptx::mbar_wait(&full[s], (it / STAGES) & 1);
           const uint32_t st = ptx::smem_u32(smem + s * Sm::stage_bytes);
-          constexpr int NTS = 32 * kSplitWarps;
-#pragma unroll 4
-          for (int i = tid; i < Sm::a_bytes / 16; i += NTS)
-            ptx::split_tf32_chunk_s(st + 16 * i, st + Sm::a_bytes + 16 * i);
-#pragma unroll 4
-          for (int i = tid; i < Sm::b_bytes / 16; i += NTS)
-            ptx::split_tf32_chunk_s(st + 2 * Sm::a_bytes + 16 * i,
-                                    st + 2 * Sm::a_bytes + Sm::b_bytes + 16 * i);
+          split_region(st, Sm::a_bytes / 16, Sm::a_bytes, tid);
+          split_region(st + 2 * Sm::a_bytes, Sm::b_bytes / 16, Sm::b_bytes, tid);
           ptx::fence_async_smem();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&sfull[s]);
