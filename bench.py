@@ -415,7 +415,7 @@ def run_gpu(args) -> None:
     # its own device and pinned-host buffers, so one call's H2D copy, another's
     # kernels and a third's D2H copy overlap.  Every call still copies its full
     # input in and its full output out inside the timed region.
-    E2E_STREAMS = 3
+    E2E_STREAMS = int(os.environ.get("WINO_E2E_STREAMS", "4"))
     e2e_streams = [stream] + [torch.cuda.Stream(device=dev) for _ in range(E2E_STREAMS - 1)]
     e2e_bufs = []
     for si in range(E2E_STREAMS):
@@ -491,7 +491,7 @@ def run_gpu(args) -> None:
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "TFLOPS", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": e2e_steps, "streams": E2E_STREAMS,
-                    "path": "wino_forward_host (C ABI), pinned host buffers, independent layer calls round-robin over 3 streams"},
+                    "path": f"wino_forward_host (C ABI), pinned host buffers, independent layer calls round-robin over {E2E_STREAMS} streams"},
             "gpu_launches": launches_step * args.steps,
             "clocks": clocks,
             "step_ms": step_ms,

@@ -22,6 +22,7 @@
 // FP64 (the reference's fp64 precision, test_engine.py:114-119) runs on a
 // small CUDA-core tiled kernel: there is no fp64 tensor-core path worth using.
 #include <cstdio>
+#include <cstdlib>
 
 #include "sm100_ptx.cuh"
 #include "wino_internal.h"
@@ -86,7 +87,7 @@ template <int PREC, int BN>
 __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
     wgemm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmU,
                     const __grid_constant__ CUtensorMap tmM, int a2, int num_kb,
-                    int kb_per_split, int n_pblk, int n_kblk, int n_units) {
+                    int kb_per_split, int n_pblk, int n_kblk, int n_units, int dbg) {
   using Tr = GemmTraits<PREC>;
   using Sm = GemmSmem<PREC, BN>;
   constexpr int STAGES = Sm::stages;
@@ -153,6 +154,7 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
           ptx::mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
           unsigned char* st = smem + s * Sm::stage_bytes;
           // HBM holds one plane; 3xTF32's lo planes are produced on chip
+          if (dbg & 2) { ptx::mbar_arrive(&full[s]); continue; }
           ptx::mbar_arrive_expect_tx(&full[s], Sm::a_bytes + Sm::b_bytes);
           ptx::tma_load_3d(st, &tmV, &full[s], kb * Tr::bk, pb * kTileP, comp);
           ptx::tma_load_3d(st + Tr::nsplit * Sm::a_bytes, &tmU, &full[s], kb * Tr::bk, kbk * BN,
@@ -187,6 +189,7 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
           const uint32_t b_lo = b_hi + Sm::b_bytes;
 #pragma unroll
           for (int k = 0; k < Tr::bk / Tr::uk; ++k) {
+            if (dbg & 8) break;
             const uint32_t off = k * 32;  // 32 bytes of K per MMA inside the swizzle atom
             const uint32_t accum = (kb != kb0 || k != 0) ? 1u : 0u;
             if constexpr (Tr::nsplit == 2) {
@@ -222,8 +225,10 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
           const int s = it % STAGES;
           ptx::mbar_wait(&full[s], (it / STAGES) & 1);
           const uint32_t st = ptx::smem_u32(smem + s * Sm::stage_bytes);
-          split_region(st, Sm::a_bytes / 16, Sm::a_bytes, tid);
-          split_region(st + 2 * Sm::a_bytes, Sm::b_bytes / 16, Sm::b_bytes, tid);
+          if (!(dbg & 4)) {
+            split_region(st, Sm::a_bytes / 16, Sm::a_bytes, tid);
+            split_region(st + 2 * Sm::a_bytes, Sm::b_bytes / 16, Sm::b_bytes, tid);
+          }
           ptx::fence_async_smem();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&sfull[s]);
@@ -251,6 +256,7 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
         ptx::tmem_ld_32x32b_x32(tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16) + c0,
                                 r);
         float* buf = buf0 + (nbuf & 1) * (kEpiBuf / 4);
+        if (dbg & 1) { ptx::tmem_ld_wait(); continue; }
         if (lane == 0) ptx::bulk_wait_read<1>();  // the store that last used `buf` has read it
         __syncwarp();
         ptx::tmem_ld_wait();
@@ -344,6 +350,13 @@ static int num_sms() {
   return n;
 }
 
+static int gemm_dbg() {  // diagnostic: 1 = skip M stores, 2 = skip operand loads,
+                         // 4 = skip the 3xTF32 split, 8 = skip the MMAs
+  static int v = -1;
+  if (v < 0) v = getenv("WINO_GEMM_DBG") ? atoi(getenv("WINO_GEMM_DBG")) : 0;
+  return v;
+}
+
 template <int PREC, int BN>
 static cudaError_t launch_tc(const GemmArgs& a, cudaStream_t s) {
   using Tr = GemmTraits<PREC>;
@@ -380,7 +393,7 @@ static cudaError_t launch_tc(const GemmArgs& a, cudaStream_t s) {
   if (units > 0x7fffffffLL) return cudaErrorInvalidValue;
   const int grid = static_cast<int>(units < num_sms() ? units : num_sms());
   launch_k(kern, dim3(grid), dim3(gemm_threads<PREC>()), Sm::total, s, tmV, tmU, tmM, a.a2, num_kb, kbps,
-           n_pblk, n_kblk, static_cast<int>(units));
+           n_pblk, n_kblk, static_cast<int>(units), gemm_dbg());
   return cudaGetLastError();
 }
 

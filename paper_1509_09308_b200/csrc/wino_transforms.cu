@@ -249,6 +249,100 @@ __global__ void __launch_bounds__(256) input_transform_kernel(
   }
 }
 
+// ----------------------------------------- whole-plane input transform (small)
+// Small images whose rows are not 16-byte aligned (VGG conv5: 14 x 14, W*4 = 56
+// bytes, so no TMA box): the CB channel planes of one image are one contiguous,
+// 16-byte-aligned run of HBM (HW % 4 == 0), read with coalesced 16-byte loads
+// into [channel][PS] shared planes (PS odd: per-lane patch reads hit distinct
+// banks).  Warp w then transforms tiles w, w+8, ... of the image's tile rows
+// that fall inside the chunk; the patch bounds are warp-uniform, so padding is
+// a uniform select, not a memory access.  Same V layout as the kernels above.
+template <int M, int PREC>
+__global__ void __launch_bounds__(256) input_transform_plane_kernel(
+    const float* __restrict__ d, void* __restrict__ V, int C, int H, int W, int pad, int th,
+    int tw, int row0, int rows, long long Pc, int c_pad, int ps) {
+  using A = Alg<M>;
+  constexpr int AL = A::alpha;
+  constexpr int CPL = InPack<PREC>::cpl;
+  constexpr int CB = 32 * CPL;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* s = reinterpret_cast<float*>(smem_raw);
+  const int n = row0 / th + blockIdx.x;
+  const int c0 = blockIdx.y * CB;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int hw = H * W;
+  griddep_launch();
+  griddep_wait();
+
+  // ---- stage CB planes (channels >= C left unread: their lanes exit below)
+  const int nch = min(CB, C - c0);
+  const float4* src = reinterpret_cast<const float4*>(d + (static_cast<size_t>(n) * C + c0) * hw);
+  const int q_per_plane = hw >> 2;
+  const int nq = nch * q_per_plane;
+  constexpr int B = 4;  // loads in flight per thread
+  for (int base = threadIdx.x; base < nq; base += 256 * B) {
+    float4 v[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int q = base + b * 256;
+      if (q < nq) v[b] = __ldg(src + q);
+    }
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int q = base + b * 256;
+      if (q < nq) {
+        const int ch = q / q_per_plane, off = (q - ch * q_per_plane) * 4;
+        float* dst = s + ch * ps + off;
+        dst[0] = v[b].x; dst[1] = v[b].y; dst[2] = v[b].z; dst[3] = v[b].w;
+      }
+    }
+  }
+  __syncthreads();
+
+  const int cbase = c0 + lane * CPL;
+  if (cbase >= C) return;
+  const int r_lo = max(row0, n * th), r_hi = min(row0 + rows, (n + 1) * th);
+  const int ntile = (r_hi - r_lo) * tw;
+  const size_t plane_v = static_cast<size_t>(AL) * AL * Pc * c_pad;
+  const size_t comp_stride = static_cast<size_t>(Pc) * c_pad;
+  for (int t = warp; t < ntile; t += 8) {
+    const int ty = r_lo - n * th + t / tw, tx = t - (t / tw) * tw;
+    const int y0 = M * ty - pad, x0 = M * tx - pad;
+    float out[CPL][AL][AL];
+#pragma unroll
+    for (int h = 0; h < CPL; ++h) {
+      const float* sc = s + (lane * CPL + h) * ps;
+      float in[AL][AL];
+#pragma unroll
+      for (int i = 0; i < AL; ++i) {
+        const int gy = y0 + i;
+        const bool rok = gy >= 0 && gy < H;
+#pragma unroll
+        for (int j = 0; j < AL; ++j) {
+          const int gx = x0 + j;
+          in[i][j] = (rok && gx >= 0 && gx < W) ? sc[gy * W + gx] : 0.f;
+        }
+      }
+      if constexpr (M == 4)
+        bt6_2d(in, out[h]);
+      else
+        sandwich<float, AL, AL>(in, out[h], [](int i, int j) { return A::BT(i, j); });
+    }
+    const long long p = static_cast<long long>(r_lo - row0) * tw + t;  // chunk-local tile
+    size_t idx = static_cast<size_t>(p) * c_pad + cbase;
+#pragma unroll
+    for (int xi = 0; xi < AL; ++xi)
+#pragma unroll
+      for (int nu = 0; nu < AL; ++nu) {
+        float v[CPL];
+#pragma unroll
+        for (int h = 0; h < CPL; ++h) v[h] = out[h][xi][nu];
+        put_ops<PREC>(V, idx, plane_v, v);
+        idx += comp_stride;
+      }
+  }
+}
+
 // ============================================================ output transform
 // One thread per (chunk tile p, filter k): reads the alpha^2 accumulators
 // M[s][comp][k][p] (coalesced over p; split-C slices summed in ascending s),
@@ -586,6 +680,32 @@ static cudaError_t input_one(const void* d, void* V, int N, int C, int H, int W,
         case 2: return input_tma_launch<M, PREC, 2>(d, V, N, C, H, W, pad, th, tw, row0, rows, Pc, c_pad, s);
         default: return input_tma_launch<M, PREC, 3>(d, V, N, C, H, W, pad, th, tw, row0, rows, Pc, c_pad, s);
       }
+    }
+  }
+  if constexpr (PREC != kFP64) {
+    // small image planes, 16-byte-aligned runs: whole-plane staging
+    constexpr int CB = 32 * InPack<PREC>::cpl;
+    const int hw = H * W;
+    const int ps = hw | 1;
+    const size_t psmem = sizeof(float) * CB * ps;
+    const long long blocks = static_cast<long long>((row0 + rows - 1) / th - row0 / th + 1) *
+                             ((C + CB - 1) / CB);
+    // enough blocks to cover the SMs (else the tile-row kernel spreads wider)
+    if (hw % 4 == 0 && psmem <= 100 * 1024 && (reinterpret_cast<uintptr_t>(d) & 15) == 0 &&
+        (blocks >= 148 || getenv("WINO_FORCE_PLANE_INPUT") != nullptr) &&
+        getenv("WINO_NO_PLANE_INPUT") == nullptr) {
+      auto kp = input_transform_plane_kernel<M, PREC>;
+      static bool pconf = false;
+      if (!pconf) {
+        cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+        max_carveout(kp);
+        pconf = true;
+      }
+      const int n0 = row0 / th, n1 = (row0 + rows - 1) / th;
+      const dim3 grid(n1 - n0 + 1, (C + CB - 1) / CB);
+      launch_k(kp, grid, dim3(256), psmem, s, static_cast<const float*>(d), V, C, H, W, pad, th,
+               tw, row0, rows, Pc, c_pad, ps);
+      return cudaGetLastError();
     }
   }
   using Cfg = InCfg<M, PREC>;

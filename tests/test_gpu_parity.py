@@ -227,3 +227,30 @@ def test_hybrid_chunked_matches_oracle(wb, monkeypatch):
         assert O.max_abs_error(y, ref) < (5e-4 if m == 2 else 5e-3)
         yo = O.winograd_forward(dn, gn, m, 1)
         assert np.abs(y - yo).max() <= 2e-5 * (1 + np.abs(yo).max())
+
+
+@pytest.mark.parametrize("force", [False, True])
+def test_plane_staged_input_transform(wb, monkeypatch, force):
+    """Small planes with rows that are not 16-byte aligned (VGG conv5: 14 x 14)
+    take the whole-plane staged input transform; forced on a row-chunked plan it
+    must also handle chunks that start and end inside an image."""
+    import torch
+    monkeypatch.setenv("WINO_PATH", "staged")
+    if force:
+        monkeypatch.setenv("WINO_FORCE_PLANE_INPUT", "1")
+    N, C, H, W, K = (80, 72, 10, 10, 16) if not force else (6, 72, 10, 10, 16)
+    cfg = wb.LayerConfig(N=N, C=C, H=H, W=W, K=K, pad=1)
+    dn = O.fill_uniform((N, C, H, W), 41)
+    gn = O.fill_uniform((K, C, 3, 3), 42)
+    d, g = torch.from_numpy(dn).cuda(), torch.from_numpy(gn).cuda()
+    ref = O.direct_forward(dn, gn, 1)
+    for m in (2, 4):
+        plan = wb.WinogradPlan(cfg, m, "fp32", workspace_limit=(96 * 1024 if force else 0))
+        if force:
+            assert plan.info["num_chunks"] > 2
+        y = plan.forward(d, g=g).cpu().numpy()
+        assert O.max_abs_error(y, ref) < (5e-4 if m == 2 else 5e-3)
+        yo = O.winograd_forward(dn, gn, m, 1)
+        assert np.abs(y - yo).max() <= 2e-5 * (1 + np.abs(yo).max())
+        yb = wb.WinogradPlan(cfg, m, "bf16").forward(d, g=g).cpu().numpy()
+        assert O.max_abs_error(yb, ref) / np.abs(ref).max() <= REL_TOL[("bf16", m)]

@@ -46,7 +46,7 @@ def timed_graph(fn, reps=20):
 
 t = timed_graph(lambda: [x.add_(1) for _ in range(200)])
 print(f"torch tiny kernel in graph: {t / 200:.2f} us/kernel")
-for (C, H, K, m, prec, N) in [(512, 14, 512, 4, "bf16", 1), (512, 14, 512, 2, "fp32", 1),
+for (C, H, K, m, prec, N) in [(16, 8, 16, 2, "fp32", 1), (16, 8, 16, 4, "bf16", 1), (512, 14, 512, 4, "bf16", 1), (512, 14, 512, 2, "fp32", 1),
                               (64, 56, 64, 2, "fp32", 1), (256, 56, 256, 4, "bf16", 1)]:
     cfg = wb.LayerConfig(N=N, C=C, H=H, W=H, K=K, pad=1)
     plan = wb.WinogradPlan(cfg, m, prec)
