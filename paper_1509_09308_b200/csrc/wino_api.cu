@@ -274,7 +274,8 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
   }
   p->bn = bn;
 
-  p->smallc = L.C <= kSmallCMax;
+  // (F(4x4) fp64 with C > 4 would exceed the small-C kernel's shared memory)
+  p->smallc = L.C <= ((prec == kFP64 && m == 4) ? 4 : kSmallCMax);
 
   // ---- chunk planner: whole tile rows, V + M staging within the budget
   const size_t budget = workspace_limit ? workspace_limit : kDefaultWorkspace;

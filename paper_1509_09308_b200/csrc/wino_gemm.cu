@@ -239,8 +239,12 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
     // ------------------------------------------------------------ epilogue
     // TMEM -> registers -> smem [32 filters][32 tiles] -> TMA bulk store into
     // M[split*a2 + comp][k][p]; the tensor map clips tiles >= Pc / filters >= K.
+    // The next 32-column TMEM load is in flight while the current one is
+    // written to shared memory (two register sets, fully unrolled), and the
+    // accumulator is released as soon as its last column is in registers.
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     float* buf0 = reinterpret_cast<float*>(smem + Sm::epi_offset + (warp - 2) * 2 * kEpiBuf);
+    const uint32_t sbuf0 = ptx::smem_u32(buf0) + 4 * lane;
     int j = 0, nbuf = 0;
     for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++j) {
       int pb, kbk, comp, split;
@@ -250,27 +254,34 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
       ptx::tc_fence_after();
       const int p0 = pb * kTileP + q * 32;
       const int z = split * a2 + comp;
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32, ++nbuf) {
-        uint32_t r[32];
-        ptx::tmem_ld_32x32b_x32(tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16) + c0,
-                                r);
-        float* buf = buf0 + (nbuf & 1) * (kEpiBuf / 4);
-        if (dbg & 1) { ptx::tmem_ld_wait(); continue; }
-        if (lane == 0) ptx::bulk_wait_read<1>();  // the store that last used `buf` has read it
-        __syncwarp();
-        ptx::tmem_ld_wait();
+      const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+      constexpr int NC = BN / 32;
+      uint32_t r[2][32];
+      ptx::tmem_ld_32x32b_x32(taddr, r[0]);
 #pragma unroll
-        for (int jj = 0; jj < 32; ++jj) buf[jj * 32 + lane] = __uint_as_float(r[jj]);
+      for (int ci = 0; ci < NC; ++ci) {
+        ptx::tmem_ld_wait();  // chunk ci in registers
+        if (ci + 1 < NC) {
+          ptx::tmem_ld_32x32b_x32(taddr + 32 * (ci + 1), r[(ci + 1) & 1]);
+        } else {
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&tempty[acc]);  // accumulator drained to registers
+        }
+        if (dbg & 1) continue;
+        const int b = nbuf++ & 1;
+        if (lane == 0) ptx::bulk_wait_read<1>();  // the store that last used buffer b has read it
+        __syncwarp();
+        const uint32_t sb = sbuf0 + b * kEpiBuf;
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj)
+          asm volatile("st.shared.b32 [%0], %1;" ::"r"(sb + jj * 128), "r"(r[ci & 1][jj]) : "memory");
         ptx::fence_async_smem();
         __syncwarp();
         if (lane == 0) {
-          ptx::tma_store_3d(&tmM, buf, p0, kbk * BN + c0, z);
+          ptx::tma_store_3d(&tmM, buf0 + b * (kEpiBuf / 4), p0, kbk * BN + 32 * ci, z);
           ptx::bulk_commit();
         }
       }
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(&tempty[acc]);
     }
     if (lane == 0) ptx::bulk_wait_all();
   }

@@ -802,216 +802,296 @@ cudaError_t launch_output_transform(int m, int prec, const void* Mbuf, void* y, 
 // ====================================================== fused tiny-C layer
 // For C <= 8 (VGG conv1.1 has C = 3) the alpha^2 GEMMs reduce over only C
 // terms, so the transform-space intermediates (alpha^2*C*P + alpha^2*K*P
-// values) dwarf the layer's input.  This kernel runs the whole layer on chip:
-// block = 32 consecutive tiles of one tile row x all K filters.
-//   1. stage the C x alpha x (32m+2) input window in smem (zero padding)
-//   2. warp c forms V[comp][c][t] = B^T d B for the 32 tiles (smem)
-//   3. filters in chunks of 32: U chunk -> smem (fp32, from the operand-format
-//      stack), thread (tile = lane, filter) forms M[comp] = sum_c U V,
-//      Y = A^T M A, and stores the m x m tile (vector rows).
+// values) dwarf the layer's input.  This kernel runs the whole layer on chip.
+// Persistent: CTA b owns the filter chunk kc = b % nkc (KC = 64 filters; its
+// alpha^2 x KC x CP transformed weights are converted to fp32 into shared
+// memory once) and strides through units = 32 consecutive tiles of one tile
+// row.  Per unit:
+//   1. the C x alpha x (32m+2) input window of the NEXT unit is requested
+//      with zero-filling cp.async (the padding is never materialised), so its
+//      load latency hides under this unit's arithmetic;
+//   2. thread (tile, channel) forms V[comp][t][c] = B^T d B (shared memory);
+//   3. two passes of 32 filters: warp = 4 filters x 32 tiles (lane = tile),
+//      M[comp] = sum_c U V from vector shared loads, the inverse transform
+//      folded per transform row xi (only the m x m outputs and two rows of
+//      Z = M A live), and the clipped m x m tile stored as vector rows.
 // Arithmetic is fp32 (fp64 for FP64): at least the precision of the
 // tensor-core path it replaces.
 constexpr int kSmallC = 8;
-constexpr int kSmallKB = 32;
+constexpr int kSmallKC = 64;   // filters per CTA
+constexpr int kSmallTiles = 32;
 
-template <int PREC>
-__device__ __forceinline__ float load_op(const void* U, size_t idx, size_t plane) {
-  if constexpr (PREC == kFP32 || PREC == kTF32) {  // fp32 (3xTF32) / tf32-rounded plane
-    return static_cast<const float*>(U)[idx];
-  } else if constexpr (PREC == kBF16) {
-    return __bfloat162float(static_cast<const __nv_bfloat16*>(U)[idx]);
+// one transformed weight in the operand format of `prec` -> fp32
+__device__ __forceinline__ float load_op_any(int prec, const void* U, size_t idx) {
+  if (prec == kBF16) return __bfloat162float(static_cast<const __nv_bfloat16*>(U)[idx]);
+  if (prec == kFP16) return __half2float(static_cast<const __half*>(U)[idx]);
+  return static_cast<const float*>(U)[idx];  // fp32 (3xTF32) / tf32-rounded plane
+}
+
+// z = A^T x for one alpha-vector (F(4,3): 10 flops with shared subexpressions;
+// F(2,3): coefficient-folded).
+template <int M, typename T>
+__device__ __forceinline__ void at_vec(const T (&x)[M + 2], T (&z)[M]) {
+  if constexpr (M == 4) {
+    const T s1 = x[1] + x[2], d1 = x[1] - x[2], s2 = x[3] + x[4], d2 = x[3] - x[4];
+    z[0] = x[0] + s1 + s2;
+    z[1] = fma(T(2), d2, d1);
+    z[2] = fma(T(4), s2, s1);
+    z[3] = fma(T(8), d2, d1) + x[5];
   } else {
-    return __half2float(static_cast<const __half*>(U)[idx]);
+    z[0] = x[0] + x[1] + x[2];
+    z[1] = x[1] - x[2] - x[3];
   }
 }
 
-// CP contiguous values (16-byte aligned) as vector shared-memory loads.
-template <typename T, int CP>
-__device__ __forceinline__ void load_vec(const T* p, T (&v)[CP]) {
-  if constexpr (sizeof(T) == 4 && CP % 4 == 0) {
+// FPW filters per warp for vector weight loads (F(2x2)'s 2x2 outputs leave
+// registers for 8, F(4x4)'s 4x4 for 4).
+template <int M, typename T>
+struct SmallCfg {
+  static constexpr int AL = M + 2, A2 = AL * AL, XW = kSmallTiles * M + 2;
+  static constexpr int FPW = (M == 2 && sizeof(T) == 4) ? 8 : 4;
+  static constexpr int passes = kSmallKC / (8 * FPW);
+};
+
+// FPW consecutive fp32 / fp64 values (16-byte aligned), broadcast loads
+template <typename T, int FPW>
+__device__ __forceinline__ void load_u(const T* p, T (&u)[FPW]) {
+  if constexpr (sizeof(T) == 4) {
 #pragma unroll
-    for (int q = 0; q < CP / 4; ++q) {
+    for (int q = 0; q < FPW / 4; ++q) {
       const float4 x = reinterpret_cast<const float4*>(p)[q];
-      v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
+      u[4 * q] = x.x; u[4 * q + 1] = x.y; u[4 * q + 2] = x.z; u[4 * q + 3] = x.w;
     }
-  } else if constexpr (sizeof(T) == 4 && CP == 2) {
-    const float2 x = *reinterpret_cast<const float2*>(p);
-    v[0] = x.x; v[1] = x.y;
   } else {
 #pragma unroll
-    for (int q = 0; q < CP / 2; ++q) {
+    for (int q = 0; q < FPW / 2; ++q) {
       const double2 x = reinterpret_cast<const double2*>(p)[q];
-      v[2 * q] = x.x; v[2 * q + 1] = x.y;
+      u[2 * q] = x.x; u[2 * q + 1] = x.y;
     }
   }
 }
 
-template <int M, int PREC, int CP>
+// CE = the exact channel count (1..4) or 8 (C = 5..8, zero-padded).
+template <int M, typename T, int CE>
 __global__ void __launch_bounds__(256, 2) fused_smallc_kernel(
-    const typename OpStore<PREC>::T* __restrict__ d, const void* __restrict__ U,
-    typename OpStore<PREC>::T* __restrict__ y, int C, int H, int W, int K, int pad, int th,
-    int tw, int oh, int ow, int c_pad) {
-  using T = typename OpStore<PREC>::T;
+    const T* __restrict__ d, const void* __restrict__ U, T* __restrict__ y, int prec, int C,
+    int H, int W, int K, int pad, int th, int tw, int oh, int ow, int c_pad, int n_units,
+    int nkc) {
   using A = Alg<M>;
-  constexpr int AL = A::alpha;
-  constexpr int A2 = AL * AL;
-  constexpr int XW = 32 * M + 2;
-  // CP = C padded to {2,4,8}: channel loops are compile-time, padded channels
-  // are zero in both the staged input and the staged filters.
-  // smem: in[CP][AL][XW] | v[A2][CP][32] | u[A2][KB][CP]
+  using Cfg = SmallCfg<M, T>;
+  constexpr int AL = Cfg::AL, A2 = Cfg::A2, XW = Cfg::XW, FPW = Cfg::FPW;
+  // smem: u[A2][CE][KC] | v[A2][CE][32] | in[2][CE][AL][XW]
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  T* s_u = reinterpret_cast<T*>(smem_raw);  // first: 16-byte aligned rows of CP values
-  T* s_v = s_u + A2 * kSmallKB * CP;
-  T* s_in = s_v + A2 * CP * 32;
+  T* s_u = reinterpret_cast<T*>(smem_raw);
+  T* s_v = s_u + A2 * CE * kSmallKC;
+  T* s_in = s_v + A2 * CE * kSmallTiles;
+  constexpr int in_elems = CE * AL * XW;
 
-  const int row = blockIdx.y;  // n*th + ty
-  const int n = row / th, ty = row - (row / th) * th;
-  const int tx0 = blockIdx.x * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int y0 = M * ty - pad, x0 = M * tx0 - pad;
+  const int kc = blockIdx.x % nkc;
+  const int k_base = kc * kSmallKC;
+  const int kn = min(kSmallKC, K - k_base);
+  const int cta = blockIdx.x / nkc, nctas = gridDim.x / nkc;
+  const int nxb = (tw + kSmallTiles - 1) / kSmallTiles;
+
+  // stage the input window of unit uu into buffer b (zero-filled cp.async)
+  auto stage = [&](int uu, int b) {
+    const int row = uu / nxb, xb = uu - (uu / nxb) * nxb;
+    const int n = row / th, ty = row - (row / th) * th;
+    const int y0 = M * ty - pad, x0 = M * xb * kSmallTiles - pad;
+    T* dst_b = s_in + b * in_elems;
+    for (int r = warp; r < CE * AL; r += 8) {  // row (c, i): lanes along x
+      const int c = r / AL, i = r - (r / AL) * AL;
+      const int gy = y0 + i;
+      const bool rowok = c < C && gy >= 0 && gy < H;
+      const T* src = d + (rowok ? ((static_cast<size_t>(n) * C + c) * H + gy) * W : 0);
+      const uint32_t dst0 = static_cast<uint32_t>(__cvta_generic_to_shared(dst_b + r * XW));
+#pragma unroll
+      for (int h = 0; h < (XW + 31) / 32; ++h) {
+        const int x = lane + 32 * h;
+        if (x >= XW) break;
+        const int gx = x0 + x;
+        const bool ok = rowok && gx >= 0 && gx < W;
+        const T* sp = ok ? src + gx : d;
+        if constexpr (sizeof(T) == 8)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst0 + 8 * x), "l"(sp),
+                       "r"(ok ? 8 : 0) : "memory");
+        else
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst0 + 4 * x), "l"(sp),
+                       "r"(ok ? 4 : 0) : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
   griddep_launch();
   griddep_wait();
-
-  for (int r = warp; r < CP * AL; r += 8) {  // row (c, i): lanes along x
-    const int c = r / AL, i = r - (r / AL) * AL;
-    const int gy = y0 + i;
-    const bool rowok = c < C && gy >= 0 && gy < H;
-    const T* src = d + (rowok ? ((static_cast<size_t>(n) * C + c) * H + gy) * W : 0);
-    for (int x = lane; x < XW; x += 32) {
-      const int gx = x0 + x;
-      s_in[r * XW + x] = (rowok && gx >= 0 && gx < W) ? __ldg(src + gx) : T(0);
+  int uu = cta;
+  if (uu < n_units) stage(uu, 0);
+  // transformed weights of this filter chunk -> fp32/fp64 smem [comp][c][k] (once)
+  for (int e = threadIdx.x; e < A2 * CE * kSmallKC; e += 256) {
+    const int kk = e % kSmallKC, r = e / kSmallKC;
+    const int c = r % CE, comp = r / CE;
+    T v = T(0);
+    if (c < C && kk < kn) {
+      const size_t idx = (static_cast<size_t>(comp) * K + k_base + kk) * c_pad + c;
+      if constexpr (sizeof(T) == 8)
+        v = static_cast<const double*>(U)[idx];
+      else
+        v = load_op_any(prec, U, idx);
     }
+    s_u[e] = v;
   }
-  __syncthreads();
-  for (int c = warp; c < CP; c += 8) {
-    T in[AL][AL], out[AL][AL];
+
+  for (int it = 0; uu < n_units; uu += nctas, ++it) {
+    const int b = it & 1;
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();  // window b landed; previous unit's s_v / window b^1 reads done
+    if (uu + nctas < n_units) stage(uu + nctas, b ^ 1);
+    const int row = uu / nxb, xb = uu - (uu / nxb) * nxb;
+    const int n = row / th, ty = row - (row / th) * th;
+    const int tx0 = xb * kSmallTiles;
+    // ---- V = B^T d B for (tile = lane, channel = warp) pairs
+    if (warp < CE) {
+      const int c = warp;
+      const T* win = s_in + b * in_elems + c * AL * XW + lane * M;
+      T in[AL][AL], out[AL][AL];
 #pragma unroll
-    for (int i = 0; i < AL; ++i)
+      for (int i = 0; i < AL; ++i)
 #pragma unroll
-      for (int j = 0; j < AL; ++j) in[i][j] = s_in[(c * AL + i) * XW + lane * M + j];
-    if constexpr (M == 4)
-      bt6_2d(in, out);
-    else
-      sandwich<T, AL, AL>(in, out, [](int i, int j) { return A::BT(i, j); });
+        for (int j = 0; j < AL; ++j) in[i][j] = win[i * XW + j];
+      if constexpr (M == 4)
+        bt6_2d(in, out);
+      else
+        sandwich<T, AL, AL>(in, out, [](int i, int j) { return A::BT(i, j); });
 #pragma unroll
-    for (int xi = 0; xi < AL; ++xi)
+      for (int xi = 0; xi < AL; ++xi)
 #pragma unroll
-      for (int nu = 0; nu < AL; ++nu) s_v[((xi * AL + nu) * 32 + lane) * CP + c] = out[xi][nu];
-  }
-  const int t = tx0 + lane;
-  const size_t plane = static_cast<size_t>(A2) * K * c_pad;
-  for (int kc = 0; kc < K; kc += kSmallKB) {
-    const int kn = min(kSmallKB, K - kc);
-    __syncthreads();  // s_v ready / previous s_u chunk consumed
-    for (int e = threadIdx.x; e < A2 * kSmallKB * CP; e += 256) {
-      const int c = e % CP, r = e / CP;
-      const int kk = r % kSmallKB, comp = r / kSmallKB;
-      T v = T(0);
-      if (c < C && kk < kn) {
-        const size_t idx = (static_cast<size_t>(comp) * K + kc + kk) * c_pad + c;
-        if constexpr (PREC == kFP64)
-          v = static_cast<const double*>(U)[idx];
-        else
-          v = load_op<PREC>(U, idx, plane);
-      }
-      s_u[e] = v;
+        for (int nu = 0; nu < AL; ++nu)
+          s_v[((xi * AL + nu) * CE + c) * kSmallTiles + lane] = out[xi][nu];
     }
     __syncthreads();
-    if (t >= tw) continue;
-    // Warp = 4 filters x 32 tiles (lane = tile).  Per component: one vector
-    // load of the tile's CP transformed channels, one broadcast vector load
-    // of each filter's CP transformed weights, 4*CP FMAs.  The inverse
-    // transform is folded per transform row xi, so only the 4 output tiles
-    // and one row of M stay live:  Z[j] = sum_nu AT[j][nu] M[xi][nu],
-    // Y[i][j] += AT[i][xi] Z[j].
-    static_assert(kSmallKB == 4 * 8, "8 warps x 4 filters per chunk");
-    const int k0 = warp * 4;
-    T out[4][M][M] = {};
+    const int t = tx0 + lane;
+    const int vr = min(M, oh - M * ty), vc = min(M, ow - M * t);
+#pragma unroll 1
+    for (int pass = 0; pass < Cfg::passes; ++pass) {
+      const int k0 = (pass * 8 + warp) * FPW;  // chunk-local first filter of this warp
+      if (k0 >= kn) break;
+      T out[FPW][M][M] = {};
+      T zp[FPW][M];  // Z of the previous transform row (F(4x4) pairs (1,2), (3,4))
 #pragma unroll
-    for (int xi = 0; xi < AL; ++xi) {
-      T mrow[4][AL];
+      for (int xi = 0; xi < AL; ++xi) {
+        T mrow[FPW][AL];
 #pragma unroll
-      for (int nu = 0; nu < AL; ++nu) {
-        const int comp = xi * AL + nu;
-        T v[CP];
-        load_vec<T, CP>(s_v + (comp * 32 + lane) * CP, v);
+        for (int nu = 0; nu < AL; ++nu) {
+          const int comp = xi * AL + nu;
 #pragma unroll
-        for (int f = 0; f < 4; ++f) {
-          T u[CP];
-          load_vec<T, CP>(s_u + (comp * kSmallKB + k0 + f) * CP, u);
-          T acc = u[0] * v[0];
+          for (int c = 0; c < CE; ++c) {
+            const T v = s_v[(comp * CE + c) * kSmallTiles + lane];
+            T u[FPW];
+            load_u<T, FPW>(s_u + (comp * CE + c) * kSmallKC + k0, u);
 #pragma unroll
-          for (int c = 1; c < CP; ++c) acc = fma(u[c], v[c], acc);
-          mrow[f][nu] = acc;
+            for (int f = 0; f < FPW; ++f) mrow[f][nu] = c == 0 ? u[f] * v : fma(u[f], v, mrow[f][nu]);
+          }
+        }
+#pragma unroll
+        for (int f = 0; f < FPW; ++f) {
+          T z[M];
+          at_vec<M, T>(mrow[f], z);
+          if constexpr (M == 4) {
+            // Y = A^T Z over xi, by pairs:  y0 = Z0 + (Z1+Z2) + (Z3+Z4),
+            // y1 = (Z1-Z2) + 2(Z3-Z4), y2 = (Z1+Z2) + 4(Z3+Z4), y3 = (Z1-Z2) + 8(Z3-Z4) + Z5
+#pragma unroll
+            for (int j = 0; j < M; ++j) {
+              if (xi == 0) {
+                out[f][0][j] = z[j];
+              } else if (xi == 1 || xi == 3) {
+                zp[f][j] = z[j];
+              } else if (xi == 2) {
+                const T sp = zp[f][j] + z[j], dm = zp[f][j] - z[j];
+                out[f][0][j] += sp;
+                out[f][1][j] = dm;
+                out[f][2][j] = sp;
+                out[f][3][j] = dm;
+              } else if (xi == 4) {
+                const T sp = zp[f][j] + z[j], dm = zp[f][j] - z[j];
+                out[f][0][j] += sp;
+                out[f][1][j] = fma(T(2), dm, out[f][1][j]);
+                out[f][2][j] = fma(T(4), sp, out[f][2][j]);
+                out[f][3][j] = fma(T(8), dm, out[f][3][j]);
+              } else {
+                out[f][3][j] += z[j];
+              }
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < M; ++i)
+#pragma unroll
+              for (int j = 0; j < M; ++j) out[f][i][j] = mac(out[f][i][j], A::AT(i, xi), z[j], false);
+          }
         }
       }
+      if (t < tw) {
 #pragma unroll
-      for (int f = 0; f < 4; ++f)
-#pragma unroll
-        for (int j = 0; j < M; ++j) {
-          T z = T(0);
-          bool first = true;
-#pragma unroll
-          for (int nu = 0; nu < AL; ++nu) {
-            const double cf = A::AT(j, nu);
-            z = mac(z, cf, mrow[f][nu], first);
-            if (cf != 0.0) first = false;
-          }
-#pragma unroll
-          for (int i = 0; i < M; ++i) out[f][i][j] = mac(out[f][i][j], A::AT(i, xi), z, false);
+        for (int f = 0; f < FPW; ++f) {
+          if (k0 + f >= kn) break;
+          const int k = k_base + k0 + f;
+          T* dst = y + ((static_cast<size_t>(n) * K + k) * oh + M * ty) * ow + M * t;
+          store_tile<M>(dst, ow, vr, vc, out[f]);
         }
-    }
-    const int vr = min(M, oh - M * ty), vc = min(M, ow - M * t);
-#pragma unroll
-    for (int f = 0; f < 4; ++f) {
-      const int k = kc + k0 + f;
-      if (k0 + f >= kn) break;
-      T* dst = y + ((static_cast<size_t>(n) * K + k) * oh + M * ty) * ow + M * t;
-      store_tile<M>(dst, ow, vr, vc, out[f]);
+      }
     }
   }
 }
 
-template <int M, int PREC, int CP>
-static cudaError_t smallc_one(const void* d, const void* U, void* y, int N, int C, int H, int W,
-                              int K, int pad, int th, int tw, int oh, int ow, int c_pad,
-                              cudaStream_t s) {
-  using T = typename OpStore<PREC>::T;
-  auto kern = fused_smallc_kernel<M, PREC, CP>;
-  constexpr int AL = M + 2, A2 = AL * AL, XW = 32 * M + 2;
-  constexpr size_t smem = sizeof(T) * (A2 * kSmallKB * CP + A2 * CP * 32 + CP * AL * XW);
-  static bool configured = false;
-  if (!configured) {
-    max_carveout(kern);
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    configured = true;
+template <int M, typename T, int CE>
+static cudaError_t smallc_one(int prec, const void* d, const void* U, void* y, int N, int C,
+                              int H, int W, int K, int pad, int th, int tw, int oh, int ow,
+                              int c_pad, cudaStream_t s) {
+  using Cfg = SmallCfg<M, T>;
+  auto kern = fused_smallc_kernel<M, T, CE>;
+  constexpr size_t smem =
+      sizeof(T) * CE * (Cfg::A2 * kSmallKC + Cfg::A2 * kSmallTiles + 2 * Cfg::AL * Cfg::XW);
+  if constexpr (smem > 227 * 1024) {  // F(4x4) fp64 with C > 4: the planner does not route here
+    return cudaErrorInvalidValue;
+  } else {
+    static bool configured = false;
+    static int per_sm = 1;
+    if (!configured) {
+      max_carveout(kern);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
+      if (per_sm < 1) per_sm = 1;
+      configured = true;
+    }
+    const int nkc = (K + kSmallKC - 1) / kSmallKC;
+    const long long units =
+        static_cast<long long>(N) * th * ((tw + kSmallTiles - 1) / kSmallTiles);
+    if (units > 0x7fffffffLL) return cudaErrorInvalidValue;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    long long per_kc = (static_cast<long long>(sms) * per_sm + nkc - 1) / nkc;
+    if (per_kc > units) per_kc = units;
+    if (per_kc < 1) per_kc = 1;
+    const dim3 grid(static_cast<unsigned>(per_kc * nkc));
+    launch_k(kern, grid, dim3(256), smem, s, static_cast<const T*>(d), U, static_cast<T*>(y),
+             prec, C, H, W, K, pad, th, tw, oh, ow, c_pad, static_cast<int>(units), nkc);
+    return cudaGetLastError();
   }
-  const dim3 grid((tw + 31) / 32, N * th);
-  launch_k(kern, grid, dim3(256), smem, s, static_cast<const T*>(d), U, static_cast<T*>(y), C, H,
-           W, K, pad, th, tw, oh, ow, c_pad);
-  return cudaGetLastError();
 }
 
-template <int M, int PREC>
-static cudaError_t smallc_cp(const void* d, const void* U, void* y, int N, int C, int H, int W,
-                             int K, int pad, int th, int tw, int oh, int ow, int c_pad,
+template <int M, typename T>
+static cudaError_t smallc_ce(int prec, const void* d, const void* U, void* y, int N, int C, int H,
+                             int W, int K, int pad, int th, int tw, int oh, int ow, int c_pad,
                              cudaStream_t s) {
-  if (C <= 2) return smallc_one<M, PREC, 2>(d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
-  if (C <= 4) return smallc_one<M, PREC, 4>(d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
-  return smallc_one<M, PREC, 8>(d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
-}
-
-template <int M>
-static cudaError_t smallc_dispatch(int prec, const void* d, const void* U, void* y, int N, int C,
-                                   int H, int W, int K, int pad, int th, int tw, int oh, int ow,
-                                   int c_pad, cudaStream_t s) {
-  switch (prec) {
-    case kFP32: return smallc_cp<M, kFP32>(d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
-    case kTF32: return smallc_cp<M, kTF32>(d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
-    case kBF16: return smallc_cp<M, kBF16>(d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
-    case kFP16: return smallc_cp<M, kFP16>(d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
-    case kFP64: return smallc_cp<M, kFP64>(d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
-    default: return cudaErrorInvalidValue;
+  switch (C) {
+    case 1: return smallc_one<M, T, 1>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
+    case 2: return smallc_one<M, T, 2>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
+    case 3: return smallc_one<M, T, 3>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
+    case 4: return smallc_one<M, T, 4>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
+    default: return smallc_one<M, T, 8>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
   }
 }
 
@@ -1019,8 +1099,11 @@ cudaError_t launch_fused_smallc(int m, int prec, const void* d, const void* U, v
                                 int C, int H, int W, int K, int pad, int th, int tw, int oh,
                                 int ow, int c_pad, cudaStream_t s) {
   if (C > kSmallC) return cudaErrorInvalidValue;
-  return m == 2 ? smallc_dispatch<2>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s)
-                : smallc_dispatch<4>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
+  if (prec == kFP64)
+    return m == 2 ? smallc_ce<2, double>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s)
+                  : smallc_ce<4, double>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
+  return m == 2 ? smallc_ce<2, float>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s)
+                : smallc_ce<4, float>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
 }
 
 // ====================================================== weight gradient

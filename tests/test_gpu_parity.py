@@ -254,3 +254,32 @@ def test_plane_staged_input_transform(wb, monkeypatch, force):
         assert np.abs(y - yo).max() <= 2e-5 * (1 + np.abs(yo).max())
         yb = wb.WinogradPlan(cfg, m, "bf16").forward(d, g=g).cpu().numpy()
         assert O.max_abs_error(yb, ref) / np.abs(ref).max() <= REL_TOL[("bf16", m)]
+
+
+@pytest.mark.parametrize("C", [1, 3, 6])
+def test_small_c_layer(wb, C):
+    """The whole-layer small-C kernel (C <= 8, VGG conv1.1): several filter
+    chunks (K = 70 > 64, partial last chunk), partial 32-tile units along x,
+    clipped edge tiles, every precision, against the fp64 direct conv and the
+    oracle's fp32 Winograd."""
+    import torch
+    N, H, W, K = 2, 19, 75, 70
+    cfg = wb.LayerConfig(N=N, C=C, H=H, W=W, K=K, pad=1)
+    dn = O.fill_uniform((N, C, H, W), 51 + C)
+    gn = O.fill_uniform((K, C, 3, 3), 52 + C)
+    ref = O.direct_forward(dn, gn, 1)
+    for m in (2, 4):
+        yo = O.winograd_forward(dn, gn, m, 1)
+        for prec in ("fp32", "tf32", "bf16", "fp16"):
+            plan = wb.WinogradPlan(cfg, m, prec)
+            assert plan.info["fused_small_c"] == 1
+            y = plan.forward(torch.from_numpy(dn).cuda(), g=torch.from_numpy(gn).cuda()).cpu().numpy()
+            if prec == "fp32":
+                assert O.max_abs_error(y, ref) < (5e-4 if m == 2 else 5e-3)
+                assert np.abs(y - yo).max() <= 2e-5 * (1 + np.abs(yo).max())
+            else:
+                assert O.max_abs_error(y, ref) / np.abs(ref).max() <= REL_TOL[(prec, m)], prec
+        if C <= 4 or m == 2:
+            d64, g64 = dn.astype(np.float64), gn.astype(np.float64)
+            y64 = _run(wb, d64, g64, 1, m)
+            assert O.max_abs_error(y64, O.direct_forward(d64, g64, 1)) < 1e-12
