@@ -546,13 +546,14 @@ cudaError_t launch_filter_transform(int m, int prec, const void* g, void* U, int
 // mod 4 columns left of the window.  It carries alpha+1 rows and XWB = 4*odd
 // columns so each channel plane is an odd number of 16-byte units: lane =
 // channel then reads its patch rows with conflict-free LDS.128.
-// Block = 32 channels x 16 tiles; warp w transforms tiles w and w+8.
+// Block = 32 channels x TPX tiles (16 for F(2x2), 8 for F(4x4): a 32-56 KB
+// box, so 4-5 blocks share an SM); warp w transforms tiles w (and w+8).
 template <int M, int SH>
 struct InTma {
   static constexpr int alpha = M + 2;
-  static constexpr int tpx = 16;
+  static constexpr int tpx = (M == 2) ? 16 : 8;
   static constexpr int rows = alpha + 1;
-  static constexpr int xwb = (M == 2) ? 44 : 76;  // >= SH + 16*M + 2, 4*odd
+  static constexpr int xwb = 44;  // >= SH + tpx*M + 2 (and the last float4 patch read), 4*odd
   static constexpr int plane = rows * xwb;
   static constexpr int bytes = 32 * plane * 4;
   static constexpr int nv = (M == 2) ? 2 : 3;     // float4 reads per patch row
@@ -615,7 +616,7 @@ __global__ void __launch_bounds__(256) input_transform_tma_kernel(
   const size_t comp_stride = static_cast<size_t>(Pc) * c_pad;
   const float* sc = s + lane * Cfg::plane;
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
+  for (int h = 0; h < Cfg::tpx / 8; ++h) {
     const int t = warp + 8 * h;
     if (tx0 + t >= tw) break;
     float in[AL][AL];
