@@ -343,6 +343,40 @@ __global__ void __launch_bounds__(256) input_transform_plane_kernel(
   }
 }
 
+// z = A^T x for one alpha-vector (F(4,3): 10 flops with shared subexpressions;
+// F(2,3): coefficient-folded).
+template <int M, typename T>
+__device__ __forceinline__ void at_vec(const T (&x)[M + 2], T (&z)[M]) {
+  if constexpr (M == 4) {
+    const T s1 = x[1] + x[2], d1 = x[1] - x[2], s2 = x[3] + x[4], d2 = x[3] - x[4];
+    z[0] = x[0] + s1 + s2;
+    z[1] = fma(T(2), d2, d1);
+    z[2] = fma(T(4), s2, s1);
+    z[3] = fma(T(8), d2, d1) + x[5];
+  } else {
+    z[0] = x[0] + x[1] + x[2];
+    z[1] = x[1] - x[2] - x[3];
+  }
+}
+
+// out = A^T in A with at_vec over the columns, then over the rows.
+template <int M, typename T>
+__device__ __forceinline__ void at_2d(const T (&in)[M + 2][M + 2], T (&out)[M][M]) {
+  constexpr int AL = M + 2;
+  T tmp[M][AL];
+#pragma unroll
+  for (int v = 0; v < AL; ++v) {
+    T col[AL], z[M];
+#pragma unroll
+    for (int u = 0; u < AL; ++u) col[u] = in[u][v];
+    at_vec<M, T>(col, z);
+#pragma unroll
+    for (int i = 0; i < M; ++i) tmp[i][v] = z[i];
+  }
+#pragma unroll
+  for (int i = 0; i < M; ++i) at_vec<M, T>(tmp[i], out[i]);
+}
+
 // ============================================================ output transform
 // One thread per (chunk tile p, filter k): reads the alpha^2 accumulators
 // M[s][comp][k][p] (coalesced over p; split-C slices summed in ascending s),
@@ -379,7 +413,7 @@ __global__ void __launch_bounds__(128, 8) output_transform_kernel(const TA* __re
       for (int nu = 0; nu < AL; ++nu) in[xi][nu] += __ldg(src + (xi * AL + nu) * cstride);
   }
   TA out[M][M];
-  sandwich<TA, M, AL>(in, out, [](int i, int j) { return A::AT(i, j); });
+  at_2d<M, TA>(in, out);
   const long long gp = static_cast<long long>(row0) * tw + p;
   const long long per_img = static_cast<long long>(th) * tw;
   const int n = static_cast<int>(gp / per_img);
@@ -399,7 +433,7 @@ constexpr int kOutTP = 128;  // tiles per block
 template <int M>
 struct OutTma {
   static constexpr int alpha = M + 2;
-  static constexpr int OF = (M == 4) ? 2 : 4;  // filters per block
+  static constexpr int OF = (M == 4) ? 1 : 4;  // filters per block (18-37 KB boxes)
   static constexpr int bytes = alpha * alpha * OF * kOutTP * 4;
 };
 
@@ -447,7 +481,7 @@ __global__ void __launch_bounds__(kOutTP) output_transform_tma_kernel(
 #pragma unroll
       for (int nu = 0; nu < AL; ++nu) in[xi][nu] = s[((xi * AL + nu) * Cfg::OF + f) * kOutTP + t];
     float out[M][M];
-    sandwich<float, M, AL>(in, out, [](int i, int j) { return A::AT(i, j); });
+    at_2d<M, float>(in, out);
     float* dst = y + ((static_cast<size_t>(n) * K + k) * oh + M * ty) * ow + M * tx;
     store_tile<M>(dst, ow, vr, vc, out);
   }
@@ -827,22 +861,6 @@ __device__ __forceinline__ float load_op_any(int prec, const void* U, size_t idx
   if (prec == kBF16) return __bfloat162float(static_cast<const __nv_bfloat16*>(U)[idx]);
   if (prec == kFP16) return __half2float(static_cast<const __half*>(U)[idx]);
   return static_cast<const float*>(U)[idx];  // fp32 (3xTF32) / tf32-rounded plane
-}
-
-// z = A^T x for one alpha-vector (F(4,3): 10 flops with shared subexpressions;
-// F(2,3): coefficient-folded).
-template <int M, typename T>
-__device__ __forceinline__ void at_vec(const T (&x)[M + 2], T (&z)[M]) {
-  if constexpr (M == 4) {
-    const T s1 = x[1] + x[2], d1 = x[1] - x[2], s2 = x[3] + x[4], d2 = x[3] - x[4];
-    z[0] = x[0] + s1 + s2;
-    z[1] = fma(T(2), d2, d1);
-    z[2] = fma(T(4), s2, s1);
-    z[3] = fma(T(8), d2, d1) + x[5];
-  } else {
-    z[0] = x[0] + x[1] + x[2];
-    z[1] = x[1] - x[2] - x[3];
-  }
 }
 
 // FPW filters per warp for vector weight loads (F(2x2)'s 2x2 outputs leave

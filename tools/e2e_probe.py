@@ -1,0 +1,61 @@
+"""Copy-only model of the bench's e2e leg: the VGG-E layer calls' H2D input and
+D2H output copies (pinned host memory), round-robin over S streams, for a few
+call orders.  Tells how close the e2e number is to the PCIe bound.
+
+usage: python tools/e2e_probe.py [BATCH]
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_1509_09308_b200.suites import VGG_E_ROWS  # noqa: E402
+
+B = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+calls = []
+for (lbl, C, H, K, depth) in VGG_E_ROWS:
+    for _ in range(depth):
+        calls.append((lbl, B * C * H * H, B * K * H * H))
+
+
+def run(order, S, steps=5):
+    streams = [torch.cuda.Stream() for _ in range(S)]
+    bufs = [[(torch.empty(i, pin_memory=True), torch.empty(i, device="cuda"),
+              torch.empty(o, device="cuda"), torch.empty(o, pin_memory=True))
+             for (_, i, o) in calls] for _ in range(S)]
+
+    def step():
+        for n, ci in enumerate(order):
+            si = n % S
+            hi, di, do, ho = bufs[si][ci]
+            with torch.cuda.stream(streams[si]):
+                di.copy_(hi, non_blocking=True)
+                ho.copy_(do, non_blocking=True)
+
+    step()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    cur = torch.cuda.current_stream()
+    a.record(cur)
+    for s in streams:
+        s.wait_stream(cur)
+    for _ in range(steps):
+        step()
+    for s in streams:
+        cur.wait_stream(s)
+    b.record(cur)
+    b.synchronize()
+    return a.elapsed_time(b) / steps
+
+
+nb_in = sum(i for _, i, _ in calls) * 4
+nb_out = sum(o for _, _, o in calls) * 4
+print(f"batch {B}: H2D {nb_in / 1e6:.1f} MB, D2H {nb_out / 1e6:.1f} MB per step")
+n = len(calls)
+orders = {"network": list(range(n)), "reversed": list(range(n))[::-1],
+          "interleaved": [x for pair in zip(range(n // 2), range(n - 1, n // 2 - 1, -1)) for x in pair]}
+for name, order in orders.items():
+    for S in (2, 4, 8):
+        ms = run(order, S)
+        print(f"{name:12s} S={S}: {ms:.3f} ms/step  ({(nb_in + nb_out) / ms / 1e6:.1f} GB/s)")
