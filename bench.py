@@ -50,16 +50,18 @@ def load_traffic(algo, prec, batch, stage):
     """Per-launch DRAM bytes of the dominant kernel from the committed ncu launch
     list for this workload (profiles/*/traffic.json), or None."""
     import glob
-    kern = {"batched_gemm": "wgemm_tc_kernel", "input_transform": "input_transform_tma_kernel",
-            "output_transform": "output_transform_kernel",
-            "filter_transform": "filter_transform_kernel"}[stage]
+    kerns = {"batched_gemm": ["wgemm_tc_kernel"],
+             "input_transform": ["input_transform_tma_kernel", "input_transform_kernel"],
+             "output_transform": ["output_transform_tma_kernel", "output_transform_kernel"],
+             "filter_transform": ["filter_transform_kernel"]}[stage]
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "traffic.json")), reverse=True):
         try:
             with open(path) as fh:
                 tab = json.load(fh)
-            hit = tab.get(f"{algo}:{prec}:N{batch}", {}).get(kern)
-            if hit is not None:
-                return hit
+            row = tab.get(f"{algo}:{prec}:N{batch}", {})
+            for kern in kerns:
+                if row.get(kern) is not None:
+                    return row[kern]
         except Exception:
             pass
     return None

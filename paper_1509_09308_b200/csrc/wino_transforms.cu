@@ -61,48 +61,64 @@ template <int M, typename TA>
 __device__ __forceinline__ void store_tile(TA* dst, int ow, int vr, int vc, const TA (&out)[M][M]);
 
 // ============================================================ filter transform
-// Block = 256 consecutive (k, c) pairs = 256 contiguous 3x3 filters: staged
-// through shared memory with coalesced loads (the 36-byte records would
-// otherwise give strided warp loads), then one thread per (k, c) writes
+// Block = 256 x FPT consecutive (k, c) pairs = contiguous 3x3 filters, staged
+// through shared memory with coalesced 16-byte loads (all of a thread's loads
+// in flight at once; the 36-byte records would otherwise give strided warp
+// loads), then thread t forms G g G^T for pairs t, t+256, ... and writes
 // U[s][comp][k][c] with c fastest (coalesced across the warp).
 // (engine.py:104-114)
-template <int M, int PREC>
+template <int M, int PREC, int FPT>
 __global__ void __launch_bounds__(256) filter_transform_kernel(
     const typename OpStore<PREC>::T* __restrict__ g, void* __restrict__ U, int K, int C,
     int c_pad) {
   using T = typename OpStore<PREC>::T;
   using A = Alg<M>;
   constexpr int AL = A::alpha;
-  __shared__ T sg[256 * 9 + 1];
+  constexpr int NP = 256 * FPT;  // pairs per block
+  __shared__ __align__(16) T sg[NP * 9];
   griddep_launch();
   griddep_wait();
   const long long total = static_cast<long long>(K) * C;
-  const long long t0 = static_cast<long long>(blockIdx.x) * 256;
-  const int nloc = static_cast<int>(min(256LL, total - t0));
+  const long long t0 = static_cast<long long>(blockIdx.x) * NP;
+  const int nloc = static_cast<int>(min(static_cast<long long>(NP), total - t0));
   const T* src = g + t0 * 9;
-  for (int e = threadIdx.x; e < nloc * 9; e += 256) sg[e] = __ldg(src + e);
+  constexpr int VE = 16 / sizeof(T);  // elements per 16-byte load
+  if (nloc == NP && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+    constexpr int NV = NP * 9 / VE / 256;  // 16-byte loads per thread
+    uint4 v[NV];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) v[q] = __ldg(reinterpret_cast<const uint4*>(src) + threadIdx.x + 256 * q);
+#pragma unroll
+    for (int q = 0; q < NV; ++q) reinterpret_cast<uint4*>(sg)[threadIdx.x + 256 * q] = v[q];
+  } else {
+    for (int e = threadIdx.x; e < nloc * 9; e += 256) sg[e] = __ldg(src + e);
+  }
   __syncthreads();
-  if (static_cast<int>(threadIdx.x) >= nloc) return;
-  const long long t = t0 + threadIdx.x;
-  const int k = static_cast<int>(t / C);
-  const int c = static_cast<int>(t - static_cast<long long>(k) * C);
-  T in[3][3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) in[i][j] = sg[threadIdx.x * 9 + i * 3 + j];
-  T out[AL][AL];
-  sandwich<T, AL, 3>(in, out, [](int i, int j) { return A::G(i, j); });
   const size_t plane = static_cast<size_t>(AL) * AL * K * c_pad;
   const size_t cstride = static_cast<size_t>(K) * c_pad;
-  size_t idx = static_cast<size_t>(k) * c_pad + c;
 #pragma unroll
-  for (int xi = 0; xi < AL; ++xi)
+  for (int q = 0; q < FPT; ++q) {
+    const int j = threadIdx.x + 256 * q;
+    if (j >= nloc) break;
+    const long long t = t0 + j;
+    const int k = static_cast<int>(t / C);
+    const int c = static_cast<int>(t - static_cast<long long>(k) * C);
+    T in[3][3];
 #pragma unroll
-    for (int nu = 0; nu < AL; ++nu) {
-      OpStore<PREC>::put(U, idx, plane, out[xi][nu]);
-      idx += cstride;
-    }
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int jj = 0; jj < 3; ++jj) in[i][jj] = sg[j * 9 + i * 3 + jj];
+    T out[AL][AL];
+    sandwich<T, AL, 3>(in, out, [](int i, int jj) { return A::G(i, jj); });
+    size_t idx = static_cast<size_t>(k) * c_pad + c;
+#pragma unroll
+    for (int xi = 0; xi < AL; ++xi)
+#pragma unroll
+      for (int nu = 0; nu < AL; ++nu) {
+        OpStore<PREC>::put(U, idx, plane, out[xi][nu]);
+        idx += cstride;
+      }
+  }
 }
 
 // ============================================================= input transform
@@ -540,13 +556,14 @@ template <int M, int PREC>
 static void filter_launch(const void* g, void* U, int K, int C, int c_pad, cudaStream_t s) {
   using T = typename OpStore<PREC>::T;
   const long long n = static_cast<long long>(K) * C;
-  auto kern = filter_transform_kernel<M, PREC>;
+  constexpr int FPT = sizeof(T) == 4 ? 4 : 2;  // 36 KB of staged filters per block
+  auto kern = filter_transform_kernel<M, PREC, FPT>;
   static bool configured = false;
   if (!configured) {
     max_carveout(kern);
     configured = true;
   }
-  launch_k(kern, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s,
+  launch_k(kern, dim3(static_cast<unsigned>((n + 256 * FPT - 1) / (256 * FPT))), dim3(256), 0, s,
            static_cast<const T*>(g), U, K, C, c_pad);
 }
 

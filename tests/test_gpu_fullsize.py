@@ -1,0 +1,89 @@
+"""Parity at BASELINE.json's full sizes (VGG-E shapes at N = 64, the
+multi-chunk, two-stream staged plans the bench times).  The fp64 direct-conv
+oracle is too slow for a whole batch, so -- images being independent (SURVEY
+sec. 8d) -- deterministic image subsets are checked against it, and
+size-independent properties cover the rest: batch-slice consistency (image n
+of the batched call equals a single-image call, which catches chunk/stream
+indexing slips) and linearity in the input.
+
+Tolerances are the same as test_gpu_parity.py: fp32 (3xTF32) max-abs vs fp64
+direct F2 < 5e-4 / F4 < 5e-3; bf16 relative to max|y| F2 2e-2 / F4 1.5e-1.
+"""
+import numpy as np
+import pytest
+
+from oracle import winograd_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def wb():
+    import paper_1509_09308_b200 as wb
+    return wb
+
+
+def _layer(wb, N, C, H, K, m, prec, seed):
+    import torch
+    cfg = wb.LayerConfig(N=N, C=C, H=H, W=H, K=K, pad=1)
+    plan = wb.WinogradPlan(cfg, m, prec)
+    gen = torch.Generator(device="cpu").manual_seed(seed)
+    d = (torch.rand((N, C, H, H), generator=gen) * 2 - 1).cuda()
+    g = (torch.rand((K, C, 3, 3), generator=gen) * 2 - 1).cuda()
+    y = plan.forward(d, g=g)
+    torch.cuda.synchronize()
+    return plan, d, g, y
+
+
+@pytest.mark.parametrize("label,C,H,K,m,prec", [
+    ("conv3.2", 256, 56, 256, 4, "bf16"),
+    ("conv3.2", 256, 56, 256, 4, "fp32"),
+    ("conv2.2", 128, 112, 128, 2, "fp32"),
+    ("conv5", 512, 14, 512, 4, "bf16"),
+])
+def test_vgg_layer_n64_image_subset(wb, label, C, H, K, m, prec):
+    plan, d, g, y = _layer(wb, 64, C, H, K, m, prec, seed=len(label) + C + m)
+    assert plan.info["num_chunks"] >= 1
+    gn = g.cpu().numpy()
+    for n in (0, 37, 63):
+        dn = d[n:n + 1].cpu().numpy()
+        ref = O.direct_forward(dn, gn, 1)
+        got = y[n:n + 1].cpu().numpy()
+        if prec == "fp32":
+            assert O.max_abs_error(got, ref) < (5e-4 if m == 2 else 5e-3), (label, n)
+        else:
+            tol = 2e-2 if m == 2 else 1.5e-1
+            assert O.max_abs_error(got, ref) / np.abs(ref).max() <= tol, (label, n)
+
+
+def test_batch_slice_consistency_conv12(wb):
+    """conv1.2 at N = 64 (42 row chunks over two streams): every image of the
+    batched call equals a single-image plan's output (same arithmetic; any
+    chunk, stream or tile-index slip would be an O(1) difference)."""
+    import torch
+    plan, d, g, y = _layer(wb, 64, 64, 224, 64, 4, "bf16", seed=7)
+    assert plan.info["num_chunks"] > 8
+    one = wb.WinogradPlan(wb.LayerConfig(N=1, C=64, H=224, W=224, K=64, pad=1), 4, "bf16")
+    for n in (0, 21, 63):
+        y1 = one.forward(d[n:n + 1].contiguous(), g=g)
+        torch.cuda.synchronize()
+        diff = (y1 - y[n:n + 1]).abs().max().item()
+        assert diff <= 1e-6 * (1 + y1.abs().max().item()), (n, diff)
+
+
+def test_linearity_conv42(wb):
+    """forward(d1 + d2) = forward(d1) + forward(d2) within three times the
+    F(2x2) fp32 gate (fp32 path, conv4.2 at N = 64, split over row chunks)."""
+    import torch
+    cfg = wb.LayerConfig(N=64, C=512, H=28, W=28, K=512, pad=1)
+    plan = wb.WinogradPlan(cfg, 2, "fp32")
+    gen = torch.Generator(device="cpu").manual_seed(3)
+    d1 = (torch.rand((64, 512, 28, 28), generator=gen) - 0.5).cuda()
+    d2 = (torch.rand((64, 512, 28, 28), generator=gen) - 0.5).cuda()
+    g = (torch.rand((512, 512, 3, 3), generator=gen) - 0.5).cuda()
+    ya = plan.forward(d1, g=g)
+    yb = plan.forward(d2, g=g)
+    yc = plan.forward(d1 + d2, g=g)
+    torch.cuda.synchronize()
+    err = (yc - ya - yb).abs().max().item()
+    assert err <= 1.5e-3, err

@@ -23,6 +23,10 @@ $T 300 ncu --set full --clock-control none --import-source on -k regex:input_tra
    -o $OUT/input_conv12_f4_bf16_n64 python tools/prof_layer.py conv1.2 4 bf16 64 1 > /dev/null 2>&1
 $T 300 ncu --set full --clock-control none --import-source on -k regex:fused_smallc -s 1 -c 1 \
    -o $OUT/smallc_conv11_f4_bf16_n64 python tools/prof_layer.py conv1.1 4 bf16 64 2 > /dev/null 2>&1
+$T 300 ncu --set full --clock-control none --import-source on -k regex:output_transform -s 12 -c 1 \
+   -o $OUT/output_conv32_f4_bf16_n64 python tools/prof_layer.py conv3.2 4 bf16 64 2 > /dev/null 2>&1
+$T 300 ncu --set full --clock-control none --import-source on -k regex:wgemm -s 12 -c 1 \
+   -o $OUT/gemm_conv32_f4_bf16_n64 python tools/prof_layer.py conv3.2 4 bf16 64 2 > /dev/null 2>&1
 WINO_PATH=hybrid $T 300 ncu --set full --clock-control none --import-source on -k regex:wfused -s 1 -c 1 \
    -o $OUT/fused_hybrid_conv32_f4_bf16_n64 python tools/prof_layer.py conv3.2 4 bf16 64 2 > /dev/null 2>&1
 ls -la $OUT
