@@ -48,25 +48,33 @@ struct GemmTraits {
 constexpr int kEpiWarps = 4;
 constexpr int kEpiBuf = 32 * 32 * 4;  // one 32-tile x 32-filter fp32 block
 
-template <int PREC, int BN>
+// TA: 3xTF32 with the A operand (V, 128 tiles) split straight into tensor
+// memory -- smem holds one A plane and the B hi/lo planes, and the MMAs read A
+// from TMEM, which takes the A traffic off the shared-memory port the split and
+// the MMAs otherwise saturate.
+template <int PREC, int BN, bool TA = false>
 struct GemmSmem {
   using Tr = GemmTraits<PREC>;
   static constexpr int a_bytes = kTileP * 128;  // 128 rows x 128 B
   static constexpr int b_bytes = BN * 128;
-  static constexpr int stage_bytes = Tr::nsplit * (a_bytes + b_bytes);
+  static constexpr int stage_bytes = TA ? a_bytes + 2 * b_bytes : Tr::nsplit * (a_bytes + b_bytes);
   static constexpr int epi_bytes = kEpiWarps * 2 * kEpiBuf;  // double-buffered per warp
   static constexpr int avail = 227 * 1024 - 1024 - 512 - epi_bytes;
   static constexpr int stages = avail / stage_bytes >= 6 ? 6 : avail / stage_bytes;
   static constexpr int epi_offset = stages * stage_bytes;
   static constexpr int bar_offset = epi_offset + epi_bytes;
   static constexpr int total = bar_offset + 512 + 1024;  // barriers + alignment slack
+  // TMEM: two BN-column accumulators (+ hi/lo A columns per stage for TA)
+  static constexpr int tmem_cols = TA ? 512 : 2 * BN;
+  static constexpr int a_tmem_col = 2 * BN;             // stage s: hi at +64 s, lo at +64 s + 32
+  static_assert(!TA || 2 * BN + 64 * stages <= 512, "TMEM budget");
 };
 
 // 3xTF32 split of `n` 16-byte chunks at shared address `hi` (lo plane `lo_off`
 // bytes further) by the kSplitWarps split warps: batches of four loads in
 // flight per thread, single chunks for the tail.
-__device__ __forceinline__ void split_region(uint32_t hi, int n, int lo_off, int tid) {
-  constexpr int NTS = 32 * kSplitWarps;
+template <int NTS = 32 * kSplitWarps>
+__device__ __forceinline__ void split_region_n(uint32_t hi, int n, int lo_off, int tid) {
   int base = 0;
   for (; base + 4 * NTS <= n; base += 4 * NTS) {
     const int i = base + tid;
@@ -77,19 +85,23 @@ __device__ __forceinline__ void split_region(uint32_t hi, int n, int lo_off, int
   }
   for (int i = base + tid; i < n; i += NTS) ptx::split_tf32_chunk_s(hi + 16 * i, hi + 16 * i + lo_off);
 }
+__device__ __forceinline__ void split_region(uint32_t hi, int n, int lo_off, int tid) {
+  split_region_n<>(hi, n, lo_off, tid);
+}
 
 // Persistent, warp-specialised tcgen05 GEMM.  Work unit = (split, comp,
 // filter block, tile block); CTAs stride through units.  The accumulator is
 // double-buffered in TMEM (2 x BN columns) so the epilogue of unit j overlaps
 // the MMAs of unit j+1.  Split-C units (small-P layers) write partial sums to
 // separate M slices that the output transform adds in a fixed order.
-template <int PREC, int BN>
+template <int PREC, int BN, bool TA>
 __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
     wgemm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmU,
                     const __grid_constant__ CUtensorMap tmM, int a2, int num_kb,
                     int kb_per_split, int n_pblk, int n_kblk, int n_units, int dbg) {
   using Tr = GemmTraits<PREC>;
-  using Sm = GemmSmem<PREC, BN>;
+  using Sm = GemmSmem<PREC, BN, TA>;
+  static_assert(!TA || PREC == kFP32, "TMEM A operand is the 3xTF32 variant");
   constexpr int STAGES = Sm::stages;
   static_assert(STAGES >= 2, "pipeline needs at least two stages");
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
@@ -122,7 +134,7 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
     for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&sfull[s], kSplitWarps);  // one per split warp
     ptx::fence_mbar_init();
   }
-  if (warp == 1) ptx::tmem_alloc(tmem_slot, 2 * BN);
+  if (warp == 1) ptx::tmem_alloc(tmem_slot, Sm::tmem_cols);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -157,7 +169,7 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
           if (dbg & 2) { ptx::mbar_arrive(&full[s]); continue; }
           ptx::mbar_arrive_expect_tx(&full[s], Sm::a_bytes + Sm::b_bytes);
           ptx::tma_load_3d(st, &tmV, &full[s], kb * Tr::bk, pb * kTileP, comp);
-          ptx::tma_load_3d(st + Tr::nsplit * Sm::a_bytes, &tmU, &full[s], kb * Tr::bk, kbk * BN,
+          ptx::tma_load_3d(st + (TA ? 1 : Tr::nsplit) * Sm::a_bytes, &tmU, &full[s], kb * Tr::bk, kbk * BN,
                            comp);
         }
       }
@@ -185,14 +197,22 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
           ptx::tc_fence_after();
           const uint32_t st = ptx::smem_u32(smem + s * Sm::stage_bytes);
           const uint32_t a_hi = st, a_lo = st + Sm::a_bytes;
-          const uint32_t b_hi = st + Tr::nsplit * Sm::a_bytes;
+          const uint32_t b_hi = st + (TA ? 1 : Tr::nsplit) * Sm::a_bytes;
           const uint32_t b_lo = b_hi + Sm::b_bytes;
+          const uint32_t ta_hi = tmem_base + Sm::a_tmem_col + 64 * s, ta_lo = ta_hi + 32;
 #pragma unroll
           for (int k = 0; k < Tr::bk / Tr::uk; ++k) {
             if (dbg & 8) break;
             const uint32_t off = k * 32;  // 32 bytes of K per MMA inside the swizzle atom
             const uint32_t accum = (kb != kb0 || k != 0) ? 1u : 0u;
-            if constexpr (Tr::nsplit == 2) {
+            if constexpr (TA) {  // A (8 tf32 columns per MMA) from tensor memory
+              ptx::umma_tf32_tmem_a(d_tmem, ta_lo + 8 * k, ptx::umma_desc_sw128(b_hi + off), idesc,
+                                    accum);
+              ptx::umma_tf32_tmem_a(d_tmem, ta_hi + 8 * k, ptx::umma_desc_sw128(b_lo + off), idesc,
+                                    1u);
+              ptx::umma_tf32_tmem_a(d_tmem, ta_hi + 8 * k, ptx::umma_desc_sw128(b_hi + off), idesc,
+                                    1u);
+            } else if constexpr (Tr::nsplit == 2) {
               ptx::umma<1>(d_tmem, ptx::umma_desc_sw128(a_lo + off),
                            ptx::umma_desc_sw128(b_hi + off), idesc, accum);
               ptx::umma<1>(d_tmem, ptx::umma_desc_sw128(a_hi + off),
@@ -225,7 +245,38 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
           const int s = it % STAGES;
           ptx::mbar_wait(&full[s], (it / STAGES) & 1);
           const uint32_t st = ptx::smem_u32(smem + s * Sm::stage_bytes);
-          if (!(dbg & 4)) {
+          if constexpr (TA) {
+            if (warp < 6 + 4) {
+              // A: thread = tile row r of its warp's TMEM lane quarter; the
+              // 128-byte row (32 channels, 128B-swizzled) -> hi / lo columns
+              const int q = warp & 3, r = 32 * q + lane;
+              const uint32_t row = st + 128 * r;
+              uint32_t hi[32], lo[32];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                float x0, x1, x2, x3;
+                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                             : "=f"(x0), "=f"(x1), "=f"(x2), "=f"(x3)
+                             : "r"(row + 16 * (j ^ (r & 7))));
+                const float xs[4] = {x0, x1, x2, x3};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  uint32_t h;
+                  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(xs[e]));
+                  hi[4 * j + e] = h;
+                  lo[4 * j + e] = __float_as_uint(xs[e] - __uint_as_float(h));
+                }
+              }
+              const uint32_t t0 = tmem_base + (static_cast<uint32_t>(32 * q) << 16) +
+                                  Sm::a_tmem_col + 64 * s;
+              ptx::tmem_st_32x32b_x32(t0, hi);
+              ptx::tmem_st_32x32b_x32(t0 + 32, lo);
+              ptx::tmem_st_wait();
+              ptx::tc_fence_before();
+            } else if (!(dbg & 4)) {  // B: hi in place, lo plane, by the other 4 warps
+              split_region_n<128>(st + Sm::a_bytes, Sm::b_bytes / 16, Sm::b_bytes, tid - 128);
+            }
+          } else if (!(dbg & 4)) {
             split_region(st, Sm::a_bytes / 16, Sm::a_bytes, tid);
             split_region(st + 2 * Sm::a_bytes, Sm::b_bytes / 16, Sm::b_bytes, tid);
           }
@@ -289,7 +340,7 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
   __syncthreads();
   if (warp == 1) {
     __syncwarp();
-    ptx::tmem_dealloc(tmem_base, 2 * BN);
+    ptx::tmem_dealloc(tmem_base, Sm::tmem_cols);
   }
 }
 
@@ -368,10 +419,10 @@ static int gemm_dbg() {  // diagnostic: 1 = skip M stores, 2 = skip operand load
   return v;
 }
 
-template <int PREC, int BN>
+template <int PREC, int BN, bool TA>
 static cudaError_t launch_tc(const GemmArgs& a, cudaStream_t s) {
   using Tr = GemmTraits<PREC>;
-  using Sm = GemmSmem<PREC, BN>;
+  using Sm = GemmSmem<PREC, BN, TA>;
   alignas(64) CUtensorMap tmV, tmU;
   const uint64_t es = Tr::esize;
   const uint64_t planes = static_cast<uint64_t>(op_splits(PREC)) * a.a2;  // planes in HBM
@@ -386,7 +437,7 @@ static cudaError_t launch_tc(const GemmArgs& a, cudaStream_t s) {
   if (!encode_tmap_3d(&tmM, -1, a.M, a.Pc, a.K, static_cast<uint64_t>(splits) * a.a2,
                       a.m_ld * 4ull, static_cast<uint64_t>(a.K) * a.m_ld * 4ull, 32, 32))
     return cudaErrorInvalidValue;
-  auto kern = wgemm_tc_kernel<PREC, BN>;
+  auto kern = wgemm_tc_kernel<PREC, BN, TA>;
   static bool configured = false;  // idempotent attribute set
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -417,11 +468,22 @@ int gemm_device_sms() { return num_sms(); }
 
 template <int PREC>
 static cudaError_t launch_prec(const GemmArgs& a, cudaStream_t s) {
+  if constexpr (PREC == kFP32) {  // 3xTF32: A operand through tensor memory (BN <= 128)
+    static const bool tmem_a = getenv("WINO_NO_TMEM_A") == nullptr;
+    if (tmem_a) {
+      switch (a.bn) {
+        case 32: return launch_tc<PREC, 32, true>(a, s);
+        case 64: return launch_tc<PREC, 64, true>(a, s);
+        case 128: return launch_tc<PREC, 128, true>(a, s);
+        default: break;
+      }
+    }
+  }
   switch (a.bn) {
-    case 32: return launch_tc<PREC, 32>(a, s);
-    case 64: return launch_tc<PREC, 64>(a, s);
-    case 128: return launch_tc<PREC, 128>(a, s);
-    case 256: return launch_tc<PREC, 256>(a, s);
+    case 32: return launch_tc<PREC, 32, false>(a, s);
+    case 64: return launch_tc<PREC, 64, false>(a, s);
+    case 128: return launch_tc<PREC, 128, false>(a, s);
+    case 256: return launch_tc<PREC, 256, false>(a, s);
     default: return cudaErrorInvalidValue;
   }
 }
