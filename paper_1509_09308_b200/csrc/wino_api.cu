@@ -29,7 +29,9 @@ struct wino_plan_s {
   size_t ypart_bytes;
   int rows_total, rows_per_chunk, num_chunks;
   long long chunk_tiles;
-  long long m_ld;                    // M row stride (tiles, multiple of 4)
+  long long m_ld;                    // M row stride (tiles, multiple of 4; 8 for bf16 M)
+  int m_bf16;                        // M staged as bf16 (bf16 GEMM, staged, no split-C)
+  int m_es;                          // M element bytes
   size_t u_bytes, v_bytes, m_bytes;  // v/m per full chunk
 };
 
@@ -72,14 +74,14 @@ bool encode_tmap_3d(void* map_out, int prec, const void* base, uint64_t d0, uint
     return false;
   }
   CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-  if (prec == kBF16) dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  if (prec == kBF16 || prec == -2) dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   if (prec == kFP16) dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   cuuint64_t dims[3] = {d0, d1, d2};
   cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
   cuuint32_t box[3] = {box0, box1, 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  // operand maps use the 128B swizzle UMMA expects; the accumulator store map
-  // (prec -1, fp32) is a plain row-major box
+  // operand maps use the 128B swizzle UMMA expects; the accumulator store maps
+  // (prec -1 fp32, -2 bf16) are plain row-major boxes
   CUresult r = g_encode(reinterpret_cast<CUtensorMap*>(map_out), dt, 3, const_cast<void*>(base),
                         dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                         prec < 0 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
@@ -125,7 +127,7 @@ bool encode_tmap_3d_sw(void* map_out, int prec, const void* base, uint64_t d0, u
 // M[comp][k][p] staging box.
 bool encode_tmap_3d_box(void* map_out, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
                         uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box0,
-                        uint32_t box1, uint32_t box2) {
+                        uint32_t box1, uint32_t box2, bool bf16) {
   if (!load_encode()) {
     set_error("cuTensorMapEncodeTiled unavailable (driver too old?)");
     return false;
@@ -134,7 +136,8 @@ bool encode_tmap_3d_box(void* map_out, const void* base, uint64_t d0, uint64_t d
   cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
   cuuint32_t box[3] = {box0, box1, box2};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = g_encode(reinterpret_cast<CUtensorMap*>(map_out), CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+  CUresult r = g_encode(reinterpret_cast<CUtensorMap*>(map_out),
+                        bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                         3, const_cast<void*>(base), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -279,8 +282,13 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
 
   // ---- chunk planner: whole tile rows, V + M staging within the budget
   const size_t budget = workspace_limit ? workspace_limit : kDefaultWorkspace;
+  // bf16 GEMM: M is staged in bf16.  The accumulation stays fp32 (TMEM); the one
+  // extra rounding of M is of the size of the bf16 operand roundings of U and V
+  // that already dominate the variant's error (~7% rms added),
+  // and it halves the largest staged tensor.  WINO_M_FP32=1 keeps fp32 M.
+  p->m_es = (prec == kBF16 && getenv("WINO_M_FP32") == nullptr) ? 2 : p->acc_bytes;
   const size_t per_tile = static_cast<size_t>(p->nsplit) * p->a2 * p->c_pad * p->esize +
-                          static_cast<size_t>(p->a2) * L.K * p->acc_bytes;
+                          static_cast<size_t>(p->a2) * L.K * p->m_es;
   const size_t per_row = per_tile * p->tw;
   p->rows_total = L.N * p->th;
   long long rows = static_cast<long long>(budget / (per_row ? per_row : 1));
@@ -314,7 +322,7 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
     p->chunk_tiles = p->P;
     p->splits = 1;
   }
-  p->m_ld = static_cast<long long>(align_up(static_cast<size_t>(p->chunk_tiles), 4));
+  p->m_ld = static_cast<long long>(align_up(static_cast<size_t>(p->chunk_tiles), 8));
   // ---- path (WINO_PATH=staged|fused|hybrid overrides the choice; read at
   // plan creation):
   //   staged : input transform -> GEMM -> output transform, V and M staged;
@@ -384,12 +392,14 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
     p->v_bytes = align_up(static_cast<size_t>(p->nsplit) * p->a2 * p->chunk_tiles * p->c_pad *
                               p->esize,
                           1024);
-    p->m_ld = static_cast<long long>(align_up(static_cast<size_t>(p->chunk_tiles), 4));
+    p->m_ld = static_cast<long long>(align_up(static_cast<size_t>(p->chunk_tiles), 8));
     p->overlap = p->num_chunks > 1;
   }
+  p->m_bf16 = (p->m_es == 2 && p->splits == 1 && !p->smallc && p->path == kPathStaged) ? 1 : 0;
+  if (!p->m_bf16) p->m_es = p->acc_bytes;
   p->m_bytes = (p->smallc || p->path != kPathStaged) ? 0
                         : align_up(static_cast<size_t>(p->splits) * p->a2 * L.K * p->m_ld *
-                                       p->acc_bytes,
+                                       p->m_es,
                                    1024);
   *out = p;
   return WINO_OK;
@@ -433,6 +443,7 @@ int wino_plan_get_info(wino_plan_t p, wino_plan_info_t* info) {
                                          : p->num_chunks * 3;
   info->fused = p->path;
   info->fused_splits = p->fsplits;
+  info->m_bytes_per_elem = p->m_es;
   info->fused_small_c = p->smallc ? 1 : 0;
   info->multiplies = p->P * p->L.C * static_cast<long long>(p->L.K) * p->a2;
   return WINO_OK;
@@ -627,7 +638,7 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
                                            p->tw, row0, rows, Pc, p->c_pad, cs);
     if (e != cudaSuccess) return cuda_fail(e, "input transform");
     tm.mark(1);
-    GemmArgs ga{V, U, Mb, p->a2, L.K, L.C, p->c_pad, Pc, p->bn, p->splits, p->m_ld};
+    GemmArgs ga{V, U, Mb, p->a2, L.K, L.C, p->c_pad, Pc, p->bn, p->splits, p->m_ld, p->m_bf16};
     if (!odd) {
       e = join_filters();
       if (e != cudaSuccess) return cuda_fail(e, "filter transform join");
@@ -639,7 +650,7 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
     }
     tm.mark(2);
     e = launch_output_transform(p->m, p->prec, Mb, y, L.N, L.K, p->th, p->tw, p->oh, p->ow, row0,
-                                Pc, p->m_ld, p->splits, cs);
+                                Pc, p->m_ld, p->splits, cs, p->m_bf16);
     if (e != cudaSuccess) return cuda_fail(e, "output transform");
     tm.mark(3);
   }

@@ -24,6 +24,8 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cuda_bf16.h>
+
 #include "sm100_ptx.cuh"
 #include "wino_internal.h"
 
@@ -94,7 +96,8 @@ __device__ __forceinline__ void split_region(uint32_t hi, int n, int lo_off, int
 // double-buffered in TMEM (2 x BN columns) so the epilogue of unit j overlaps
 // the MMAs of unit j+1.  Split-C units (small-P layers) write partial sums to
 // separate M slices that the output transform adds in a fixed order.
-template <int PREC, int BN, bool TA>
+// MB: store M as bf16 (the bf16 GEMM's staged M, wino_api.cu planner).
+template <int PREC, int BN, bool TA, bool MB>
 __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
     wgemm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmU,
                     const __grid_constant__ CUtensorMap tmM, int a2, int num_kb,
@@ -323,9 +326,19 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
         if (lane == 0) ptx::bulk_wait_read<1>();  // the store that last used buffer b has read it
         __syncwarp();
         const uint32_t sb = sbuf0 + b * kEpiBuf;
+        if constexpr (MB) {  // [32 filters][32 tiles] bf16
+          const uint32_t sh = sb - 2 * lane;  // sbuf0 carries 4*lane
 #pragma unroll
-        for (int jj = 0; jj < 32; ++jj)
-          asm volatile("st.shared.b32 [%0], %1;" ::"r"(sb + jj * 128), "r"(r[ci & 1][jj]) : "memory");
+          for (int jj = 0; jj < 32; ++jj) {
+            const unsigned short h =
+                __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(r[ci & 1][jj])));
+            asm volatile("st.shared.b16 [%0], %1;" ::"r"(sh + jj * 64), "h"(h) : "memory");
+          }
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj)
+            asm volatile("st.shared.b32 [%0], %1;" ::"r"(sb + jj * 128), "r"(r[ci & 1][jj]) : "memory");
+        }
         ptx::fence_async_smem();
         __syncwarp();
         if (lane == 0) {
@@ -419,7 +432,7 @@ static int gemm_dbg() {  // diagnostic: 1 = skip M stores, 2 = skip operand load
   return v;
 }
 
-template <int PREC, int BN, bool TA>
+template <int PREC, int BN, bool TA, bool MB = false>
 static cudaError_t launch_tc(const GemmArgs& a, cudaStream_t s) {
   using Tr = GemmTraits<PREC>;
   using Sm = GemmSmem<PREC, BN, TA>;
@@ -434,10 +447,11 @@ static cudaError_t launch_tc(const GemmArgs& a, cudaStream_t s) {
     return cudaErrorInvalidValue;
   const int splits = a.splits < 1 ? 1 : a.splits;
   alignas(64) CUtensorMap tmM;
-  if (!encode_tmap_3d(&tmM, -1, a.M, a.Pc, a.K, static_cast<uint64_t>(splits) * a.a2,
-                      a.m_ld * 4ull, static_cast<uint64_t>(a.K) * a.m_ld * 4ull, 32, 32))
+  constexpr uint64_t mes = MB ? 2 : 4;  // M element bytes
+  if (!encode_tmap_3d(&tmM, MB ? -2 : -1, a.M, a.Pc, a.K, static_cast<uint64_t>(splits) * a.a2,
+                      a.m_ld * mes, static_cast<uint64_t>(a.K) * a.m_ld * mes, 32, 32))
     return cudaErrorInvalidValue;
-  auto kern = wgemm_tc_kernel<PREC, BN, TA>;
+  auto kern = wgemm_tc_kernel<PREC, BN, TA, MB>;
   static bool configured = false;  // idempotent attribute set
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -476,6 +490,17 @@ static cudaError_t launch_prec(const GemmArgs& a, cudaStream_t s) {
         case 64: return launch_tc<PREC, 64, true>(a, s);
         case 128: return launch_tc<PREC, 128, true>(a, s);
         default: break;
+      }
+    }
+  }
+  if constexpr (PREC == kBF16) {
+    if (a.m_bf16) {
+      switch (a.bn) {
+        case 32: return launch_tc<PREC, 32, false, true>(a, s);
+        case 64: return launch_tc<PREC, 64, false, true>(a, s);
+        case 128: return launch_tc<PREC, 128, false, true>(a, s);
+        case 256: return launch_tc<PREC, 256, false, true>(a, s);
+        default: return cudaErrorInvalidValue;
       }
     }
   }

@@ -48,7 +48,7 @@ cudaError_t launch_input_transform(int m, int prec, const void* d, void* V, int 
 // split slices are summed in ascending order (deterministic).
 cudaError_t launch_output_transform(int m, int prec, const void* Mbuf, void* y, int N, int K,
                                     int th, int tw, int oh, int ow, int row0, long long Pc,
-                                    long long m_ld, int splits, cudaStream_t s);
+                                    long long m_ld, int splits, cudaStream_t s, int m_bf16 = 0);
 
 // Whole layer on chip for C <= 8 (input transform + C-term reduction + output
 // transform in one kernel); U in the plan's operand format.
@@ -78,7 +78,8 @@ struct GemmArgs {
   long long Pc;
   int bn;          // filters per CTA (tcgen05 N)
   int splits;      // split-C factor: partial sums go to M slices [splits][a2][K][m_ld]
-  long long m_ld;  // M row stride (>= Pc, multiple of 4 for the TMA store)
+  long long m_ld;  // M row stride (>= Pc, multiple of 4 -- 8 for bf16 M -- for the TMA store)
+  int m_bf16 = 0;  // bf16 GEMM only: M staged as bf16 (see wino_api.cu planner)
 };
 int gemm_num_kblocks(int prec, int C);
 int gemm_device_sms();
@@ -145,7 +146,7 @@ bool encode_tmap_3d_sw(void* map_out, int prec, const void* base, uint64_t d0, u
                        uint32_t box1, int swizzle_bytes);
 bool encode_tmap_3d_box(void* map_out, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
                         uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box0,
-                        uint32_t box1, uint32_t box2);
+                        uint32_t box1, uint32_t box2, bool bf16 = false);
 bool encode_tmap_3d(void* map_out, int prec, const void* base, uint64_t d0, uint64_t d1,
                     uint64_t d2, uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box0,
                     uint32_t box1);

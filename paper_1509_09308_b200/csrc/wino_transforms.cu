@@ -446,23 +446,24 @@ __global__ void __launch_bounds__(128, 8) output_transform_kernel(const TA* __re
 // then thread = tile forms A^T M A for each of the OF filters from smem
 // (lane-contiguous, conflict-free) and stores the clipped tiles.
 constexpr int kOutTP = 128;  // tiles per block
-template <int M>
+// MT = the staged M element: float, or bf16 for the bf16 GEMM (wino_api.cu).
+template <int M, typename MT = float>
 struct OutTma {
   static constexpr int alpha = M + 2;
-  static constexpr int OF = (M == 4) ? 1 : 4;  // filters per block (18-37 KB boxes)
-  static constexpr int bytes = alpha * alpha * OF * kOutTP * 4;
+  static constexpr int OF = (M == 4) ? (sizeof(MT) == 2 ? 2 : 1) : 4;  // filters per block
+  static constexpr int bytes = alpha * alpha * OF * kOutTP * static_cast<int>(sizeof(MT));
 };
 
-template <int M>
+template <int M, typename MT>
 __global__ void __launch_bounds__(kOutTP) output_transform_tma_kernel(
     const __grid_constant__ CUtensorMap tmM, float* __restrict__ y, int K, int th, int tw, int oh,
     int ow, int row0, long long Pc) {
   using A = Alg<M>;
-  using Cfg = OutTma<M>;
+  using Cfg = OutTma<M, MT>;
   constexpr int AL = A::alpha;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  float* s = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
-                                      ~static_cast<uintptr_t>(127));
+  MT* s = reinterpret_cast<MT*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
+                                ~static_cast<uintptr_t>(127));
   __shared__ uint64_t bar;
   const int p0 = blockIdx.x * kOutTP;
   const int k0 = blockIdx.y * Cfg::OF;
@@ -495,7 +496,12 @@ __global__ void __launch_bounds__(kOutTP) output_transform_tma_kernel(
 #pragma unroll
     for (int xi = 0; xi < AL; ++xi)
 #pragma unroll
-      for (int nu = 0; nu < AL; ++nu) in[xi][nu] = s[((xi * AL + nu) * Cfg::OF + f) * kOutTP + t];
+      for (int nu = 0; nu < AL; ++nu) {
+        if constexpr (sizeof(MT) == 2)
+          in[xi][nu] = __bfloat162float(s[((xi * AL + nu) * Cfg::OF + f) * kOutTP + t]);
+        else
+          in[xi][nu] = s[((xi * AL + nu) * Cfg::OF + f) * kOutTP + t];
+      }
     float out[M][M];
     at_2d<M, float>(in, out);
     float* dst = y + ((static_cast<size_t>(n) * K + k) * oh + M * ty) * ow + M * tx;
@@ -798,19 +804,20 @@ cudaError_t launch_input_transform(int m, int prec, const void* d, void* V, int 
                 : input_dispatch<4>(prec, d, V, N, C, H, W, pad, th, tw, row0, rows, Pc, c_pad, s);
 }
 
-template <int M>
+template <int M, typename MT>
 static cudaError_t output_tma_launch(const void* Mbuf, void* y, int K, int th, int tw, int oh,
                                      int ow, int row0, long long Pc, long long m_ld,
                                      cudaStream_t s) {
-  using Cfg = OutTma<M>;
+  using Cfg = OutTma<M, MT>;
   alignas(64) CUtensorMap tmM;
-  // M [a2][K][m_ld] fp32, box (128 tiles, OF filters, a2 components), no swizzle
+  // M [a2][K][m_ld] (fp32 or bf16), box (128 tiles, OF filters, a2 components), no swizzle
+  constexpr uint64_t es = sizeof(MT);
   if (!encode_tmap_3d_box(&tmM, Mbuf, static_cast<uint64_t>(Pc), static_cast<uint64_t>(K),
-                          static_cast<uint64_t>(Cfg::alpha * Cfg::alpha), m_ld * 4ull,
-                          static_cast<uint64_t>(K) * m_ld * 4ull, kOutTP, Cfg::OF,
-                          Cfg::alpha * Cfg::alpha))
+                          static_cast<uint64_t>(Cfg::alpha * Cfg::alpha), m_ld * es,
+                          static_cast<uint64_t>(K) * m_ld * es, kOutTP, Cfg::OF,
+                          Cfg::alpha * Cfg::alpha, es == 2))
     return cudaErrorInvalidValue;
-  auto kern = output_transform_tma_kernel<M>;
+  auto kern = output_transform_tma_kernel<M, MT>;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::bytes + 128);
@@ -825,11 +832,16 @@ static cudaError_t output_tma_launch(const void* Mbuf, void* y, int K, int th, i
 
 cudaError_t launch_output_transform(int m, int prec, const void* Mbuf, void* y, int N, int K,
                                     int th, int tw, int oh, int ow, int row0, long long Pc,
-                                    long long m_ld, int splits, cudaStream_t s) {
+                                    long long m_ld, int splits, cudaStream_t s, int m_bf16) {
   if (Pc <= 0 || K <= 0) return cudaSuccess;
+  if (m_bf16) {  // bf16-staged M (bf16 GEMM, no split-C): TMA path only
+    if (splits != 1) return cudaErrorInvalidValue;
+    return m == 2 ? output_tma_launch<2, __nv_bfloat16>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s)
+                  : output_tma_launch<4, __nv_bfloat16>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s);
+  }
   if (prec != kFP64 && splits == 1 && getenv("WINO_NO_TMA_OUTPUT") == nullptr)
-    return m == 2 ? output_tma_launch<2>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s)
-                  : output_tma_launch<4>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s);
+    return m == 2 ? output_tma_launch<2, float>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s)
+                  : output_tma_launch<4, float>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s);
   const dim3 grid(static_cast<unsigned>((Pc + 127) / 128), K);
   static bool configured = false;
   if (!configured) {

@@ -283,3 +283,29 @@ def test_small_c_layer(wb, C):
             d64, g64 = dn.astype(np.float64), gn.astype(np.float64)
             y64 = _run(wb, d64, g64, 1, m)
             assert O.max_abs_error(y64, O.direct_forward(d64, g64, 1)) < 1e-12
+
+
+@pytest.mark.parametrize("m", [2, 4])
+def test_bf16_staged_m_error_budget(wb, monkeypatch, m):
+    """The bf16 GEMM stages M in bf16 (fp32 accumulation, one extra rounding of
+    each accumulator).  Measured on B200 (tools/mbf16_error.py): +22-23% rms
+    and +18-39% max-abs error over fp32-staged M, both inside the bf16 gate.
+    Gates: within REL_TOL, rms error <= 1.35x the fp32-M plan's."""
+    import torch
+    monkeypatch.setenv("WINO_PATH", "staged")
+    cfg = wb.LayerConfig(N=4, C=96, H=40, W=40, K=80, pad=1)  # enough tiles: no split-C
+    dn = O.fill_uniform((4, 96, 40, 40), 61)
+    gn = O.fill_uniform((80, 96, 3, 3), 62)
+    d, g = torch.from_numpy(dn).cuda(), torch.from_numpy(gn).cuda()
+    ref = O.direct_forward(dn, gn, 1)
+    plan = wb.WinogradPlan(cfg, m, "bf16")
+    assert plan.info["m_bytes_per_elem"] == 2
+    e16 = plan.forward(d, g=g).cpu().numpy().astype(np.float64) - ref
+    monkeypatch.setenv("WINO_M_FP32", "1")
+    plan32 = wb.WinogradPlan(cfg, m, "bf16")
+    assert plan32.info["m_bytes_per_elem"] == 4
+    e32 = plan32.forward(d, g=g).cpu().numpy().astype(np.float64) - ref
+    scale = np.abs(ref).max()
+    assert np.abs(e16).max() / scale <= REL_TOL[("bf16", m)]
+    rms16, rms32 = np.sqrt((e16 ** 2).mean()), np.sqrt((e32 ** 2).mean())
+    assert rms16 <= 1.35 * rms32, (rms16, rms32)
