@@ -66,6 +66,18 @@ class Report:
                                   for v in r))
         return "\n".join(lines) + "\n"
 
+    def to_text(self) -> str:
+        def fmt(v):
+            if v is None:
+                return "-"
+            return f"{v:.4g}" if isinstance(v, float) else str(v)
+        cells = [list(self.columns)] + [[fmt(v) for v in r] for r in self.rows]
+        widths = [max(len(row[i]) for row in cells) for i in range(len(self.columns))]
+        out = [] if self.seed is None else [f"# seed={self.seed}"]
+        for row in cells:
+            out.append("  ".join(c.rjust(w) for c, w in zip(row, widths)))
+        return "\n".join(out) + "\n"
+
 
 def cmd_bench(suite: str = "vgg-e", algo: str = "f2x2", batch: int = 1, repeats: int = 3,
               scale: float = 1.0, seed: int = 0) -> Report:

@@ -193,3 +193,22 @@ def test_filter_cache_key_semantics():
     assert k1 != engine.FilterCache._key(rand((2, 3, 3, 3), 2), alg, "fp32")
     assert k1 != engine.FilterCache._key(g, alg, "bf16")
     assert k1 != engine.FilterCache._key(g, wb.builtin(2, 3), "fp32")
+
+
+def test_cli_bench_usage_errors():
+    """The bench CLI maps domain errors to exit code 1 (reference cli.py:150-159)."""
+    from paper_1509_09308_b200.__main__ import main
+    assert main(["bench", "--algo", "fft"]) == 1
+    assert main(["bench", "--algo", "f4x4:int8"]) == 1
+    assert main(["bench", "--batch", "0"]) == 1
+
+
+def test_report_text_and_csv():
+    from paper_1509_09308_b200.commands import Report
+    r = Report(columns=("layer", "algo", "batch", "msec", "effective_gflops"), seed=3)
+    r.add("conv1.1", "f4x4", 1, 0.5, 123.25)
+    r.add("conv1.2", "f4x4", 1, None, None)
+    assert r.to_csv().splitlines()[0] == "# seed=3"
+    assert "conv1.1,f4x4,1,0.5,123.25" in r.to_csv()
+    txt = r.to_text()
+    assert "conv1.1" in txt and "123.2" in txt and "-" in txt.splitlines()[-1]
