@@ -24,7 +24,8 @@ struct wino_plan_s {
   int bn, splits;
   bool smallc;  // whole layer in the fused tiny-C kernel (no V/M staging)
   int path;     // kPathStaged / kPathFused / kPathHybrid (see plan_create)
-  bool overlap; // staged, several chunks: two chunks in flight on two streams
+  bool overlap; // staged, several chunks: nbuf chunks in flight on nbuf streams
+  int nbuf;     // V/M buffer sets (1, or the streams in flight: 2 default, 3 by env)
   int fsplits;  // split-C factor of the fused kernel
   size_t ypart_bytes;
   int rows_total, rows_per_chunk, num_chunks;
@@ -383,8 +384,12 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
   // input transform runs under chunk i's GEMM and output transform, on a second
   // stream), each with half the budget so both stay L2-resident.
   p->overlap = false;
+  p->nbuf = 1;
   if (p->path == kPathStaged && !p->smallc && p->num_chunks > 1) {
-    long long r2 = static_cast<long long>((budget / 2) / (per_row ? per_row : 1));
+    int ns = 2;
+    if (const char* e = getenv("WINO_CHUNK_STREAMS")) ns = atoi(e) == 3 ? 3 : 2;
+    p->nbuf = ns;
+    long long r2 = static_cast<long long>((budget / ns) / (per_row ? per_row : 1));
     if (r2 < 1) r2 = 1;
     p->rows_per_chunk = static_cast<int>(r2);
     p->num_chunks = (p->rows_total + p->rows_per_chunk - 1) / p->rows_per_chunk;
@@ -394,6 +399,7 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
                           1024);
     p->m_ld = static_cast<long long>(align_up(static_cast<size_t>(p->chunk_tiles), 8));
     p->overlap = p->num_chunks > 1;
+    if (!p->overlap) p->nbuf = 1;
   }
   p->m_bf16 = (p->m_es == 2 && p->splits == 1 && !p->smallc && p->path == kPathStaged) ? 1 : 0;
   if (!p->m_bf16) p->m_es = p->acc_bytes;
@@ -435,7 +441,7 @@ int wino_plan_get_info(wino_plan_t p, wino_plan_info_t* info) {
   info->chunk_tiles = p->chunk_tiles;
   info->u_bytes = p->u_bytes;
   info->workspace_bytes =
-      p->u_bytes + (p->overlap ? 2 : 1) * (p->v_bytes + p->m_bytes) + p->ypart_bytes;
+      p->u_bytes + p->nbuf * (p->v_bytes + p->m_bytes) + p->ypart_bytes;
   info->launches_per_forward =
       p->smallc ? 1
                 : p->path == kPathFused  ? 1 + (p->fsplits > 1)
@@ -498,6 +504,8 @@ namespace {
 struct SideStream {
   cudaStream_t st = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
+  cudaStream_t st2 = nullptr;      // third chunk stream (created on first use)
+  cudaEvent_t join2 = nullptr;
 };
 // One side stream per (host thread, device, caller stream): callers that
 // pipeline independent forwards on several streams must not be coupled
@@ -540,7 +548,7 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
   StageTimer tm(s, timer);
   unsigned char* ws = static_cast<unsigned char*>(workspace);
   size_t need =
-      (p->overlap ? 2 : 1) * (p->v_bytes + p->m_bytes) + p->ypart_bytes + (U ? 0 : p->u_bytes);
+      p->nbuf * (p->v_bytes + p->m_bytes) + p->ypart_bytes + (U ? 0 : p->u_bytes);
   if (workspace_bytes < need) {
     set_error("workspace too small: %zu < %zu bytes", workspace_bytes, need);
     return WINO_EINVAL;
@@ -572,6 +580,17 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
     tm.mark(0);
     U = ws;
     ws += p->u_bytes;
+  }
+  int nstreams = (chunk_overlap && side) ? p->nbuf : 1;
+  if (nstreams == 3) {  // third chunk stream: after the caller's prior work and U
+    cudaError_t e = cudaSuccess;
+    if (!side->st2) {
+      e = cudaStreamCreateWithFlags(&side->st2, cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&side->join2, cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(side->st2, side->fork, 0);
+    if (e == cudaSuccess && filt_side) e = cudaStreamWaitEvent(side->st2, side->join, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "third chunk stream");
   }
   auto join_filters = [&]() -> cudaError_t {
     if (!filt_side) return cudaSuccess;
@@ -628,11 +647,13 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
     const int rows = (row0 + p->rows_per_chunk <= p->rows_total) ? p->rows_per_chunk
                                                                   : p->rows_total - row0;
     const long long Pc = static_cast<long long>(rows) * p->tw;
-    // odd chunks on the side stream with the second V/M buffer (stream order
-    // serialises chunk i and i+2, which share a buffer; U precedes on `side`)
-    const bool odd = chunk_overlap && side && (ch & 1);
-    cudaStream_t cs = odd ? side->st : s;
-    unsigned char* V = ws + (odd ? vm : 0);
+    // chunk ch on stream ch % nbuf with V/M buffer ch % nbuf (stream order
+    // serialises chunks that share a buffer; U precedes on `side`, and the
+    // third stream waited for it at the fork)
+    const int bi = (chunk_overlap && side) ? ch % nstreams : 0;
+    const bool odd = bi != 0;
+    cudaStream_t cs = bi == 0 ? s : bi == 1 ? side->st : side->st2;
+    unsigned char* V = ws + bi * vm;
     unsigned char* Mb = V + p->v_bytes;
     cudaError_t e = launch_input_transform(p->m, p->prec, d, V, L.N, L.C, L.H, L.W, L.pad, p->th,
                                            p->tw, row0, rows, Pc, p->c_pad, cs);
@@ -654,9 +675,13 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
     if (e != cudaSuccess) return cuda_fail(e, "output transform");
     tm.mark(3);
   }
-  if (side && (chunk_overlap || filt_side)) {  // join the side stream back into `s`
+  if (side && (chunk_overlap || filt_side)) {  // join the side stream(s) back into `s`
     cudaError_t e = cudaEventRecord(side->join, side->st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(s, side->join, 0);
+    if (e == cudaSuccess && nstreams == 3) {
+      e = cudaEventRecord(side->join2, side->st2);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(s, side->join2, 0);
+    }
     if (e != cudaSuccess) return cuda_fail(e, "side stream join");
   }
   return WINO_OK;
