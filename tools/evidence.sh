@@ -9,6 +9,7 @@ $T 400 python bench.py > $OUT/bench_default.json 2> $OUT/bench_default.err
 $T 400 python bench.py --algo f4x4 --prec bf16 --batch 64 --no-cpu-baseline > $OUT/bench_f4_bf16_n64.json 2> $OUT/bench_f4.err
 $T 300 python bench.py --algo f4x4-fx --prec bf16 --no-cpu-baseline > $OUT/bench_f4fx_bf16_n1.json 2>> $OUT/bench_f4.err
 $T 400 python bench.py --algo f2x2 --batch 64 --no-cpu-baseline > $OUT/bench_f2_fp32_n64.json 2>> $OUT/bench_f4.err
+$T 400 python bench.py --algo f4x4 --prec tf32 --batch 64 --no-cpu-baseline > $OUT/bench_f4_tf32_n64.json 2>> $OUT/bench_f4.err
 $T 400 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_reference.json 2> $OUT/bench_reference.err
 # launch list of the default bench (every kernel: device time + dram bytes)
 $T 400 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
