@@ -145,9 +145,11 @@ struct InCfg {
   static constexpr int plane = alpha * xw + 1;  // odd stride: conflict-free per-lane reads
 };
 
-template <int PREC>
+template <int PREC, int CPL = InPack<PREC>::cpl>
 __device__ __forceinline__ void put_ops(void* base, size_t idx, size_t plane, const float* v) {
-  if constexpr (PREC == kBF16) {
+  if constexpr (CPL == 1) {
+    OpStore<PREC>::put(base, idx, plane, v[0]);
+  } else if constexpr (PREC == kBF16) {
     *reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(base) + idx) =
         __floats2bfloat162_rn(v[0], v[1]);
   } else if constexpr (PREC == kFP16) {
@@ -273,13 +275,12 @@ __global__ void __launch_bounds__(256) input_transform_kernel(
 // banks).  Warp w then transforms tiles w, w+8, ... of the image's tile rows
 // that fall inside the chunk; the patch bounds are warp-uniform, so padding is
 // a uniform select, not a memory access.  Same V layout as the kernels above.
-template <int M, int PREC>
+template <int M, int PREC, int CPL>
 __global__ void __launch_bounds__(256) input_transform_plane_kernel(
     const float* __restrict__ d, void* __restrict__ V, int C, int H, int W, int pad, int th,
     int tw, int row0, int rows, long long Pc, int c_pad, int ps) {
   using A = Alg<M>;
   constexpr int AL = A::alpha;
-  constexpr int CPL = InPack<PREC>::cpl;
   constexpr int CB = 32 * CPL;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* s = reinterpret_cast<float*>(smem_raw);
@@ -353,7 +354,7 @@ __global__ void __launch_bounds__(256) input_transform_plane_kernel(
         float v[CPL];
 #pragma unroll
         for (int h = 0; h < CPL; ++h) v[h] = out[h][xi][nu];
-        put_ops<PREC>(V, idx, plane_v, v);
+        put_ops<PREC, CPL>(V, idx, plane_v, v);
         idx += comp_stride;
       }
   }
@@ -741,8 +742,10 @@ static cudaError_t input_one(const void* d, void* V, int N, int C, int H, int W,
     }
   }
   if constexpr (PREC != kFP64) {
-    // small image planes, 16-byte-aligned runs: whole-plane staging
-    constexpr int CB = 32 * InPack<PREC>::cpl;
+    // small image planes, 16-byte-aligned runs: whole-plane staging (2 channels
+    // per lane for 16-bit operands: packed stores; measured faster than 1)
+    constexpr int CPL = InPack<PREC>::cpl;
+    constexpr int CB = 32 * CPL;
     const int hw = H * W;
     const int ps = hw | 1;
     const size_t psmem = sizeof(float) * CB * ps;
@@ -752,7 +755,7 @@ static cudaError_t input_one(const void* d, void* V, int N, int C, int H, int W,
     if (hw % 4 == 0 && psmem <= 100 * 1024 && (reinterpret_cast<uintptr_t>(d) & 15) == 0 &&
         (blocks >= 148 || getenv("WINO_FORCE_PLANE_INPUT") != nullptr) &&
         getenv("WINO_NO_PLANE_INPUT") == nullptr) {
-      auto kp = input_transform_plane_kernel<M, PREC>;
+      auto kp = input_transform_plane_kernel<M, PREC, CPL>;
       static bool pconf = false;
       if (!pconf) {
         cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
