@@ -307,10 +307,26 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
     const int num_kb = gemm_num_kblocks(prec, L.C);
     const long long units = ((p->chunk_tiles + 127) / 128) * ((L.K + p->bn - 1) / p->bn) * p->a2;
     if (units < sms && num_kb > 1) {
-      int sp = static_cast<int>((sms + units - 1) / units);
-      if (sp > num_kb) sp = num_kb;
-      const int kbps = (num_kb + sp - 1) / sp;
-      p->splits = (num_kb + kbps - 1) / kbps;
+      // waves x k-steps per unit (+2 for the unit's fill and epilogue) + half a
+      // k-step per M slice the output transform sums; ties -> fewer splits
+      double best = 1e30;
+      for (int sp = 1; sp <= num_kb && sp <= 8; ++sp) {
+        const int kbps = (num_kb + sp - 1) / sp;
+        const int sp_eff = (num_kb + kbps - 1) / kbps;
+        const long long waves = (units * sp_eff + sms - 1) / sms;
+        const double cost = static_cast<double>(waves) * (kbps + 2) + 0.5 * sp_eff;
+        if (cost < best - 1e-9) {
+          best = cost;
+          p->splits = sp_eff;
+        }
+      }
+      if (const char* e = getenv("WINO_SPLITS")) {  // tuning override
+        const int v = atoi(e);
+        if (v >= 1 && v <= num_kb) {
+          const int kbps = (num_kb + v - 1) / v;
+          p->splits = (num_kb + kbps - 1) / kbps;
+        }
+      }
     }
   }
   p->v_bytes = p->smallc ? 0
