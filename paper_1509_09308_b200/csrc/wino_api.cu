@@ -584,15 +584,32 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
                  cudaStreamWaitEvent(side->st, side->fork, 0) != cudaSuccess))
       side = nullptr;
   }
+  // Single-chunk staged plans whose filter transform outweighs the input
+  // transform (K > P: the deep, small-image layers at small N) swap the two:
+  // the input transform goes to the side stream and the filter transform stays
+  // in-stream, so the GEMM launches programmatically (PDL) behind the longer of
+  // the two instead of behind an event join.
+  bool in_side = false;
   if (!U) {
+    in_side = side && p->path == kPathStaged && p->num_chunks == 1 && !chunk_overlap &&
+              static_cast<long long>(p->L.K) > p->P;
+    if (in_side) {
+      cudaError_t e = launch_input_transform(p->m, p->prec, d, ws + p->u_bytes, p->L.N, p->L.C,
+                                             p->L.H, p->L.W, p->L.pad, p->th, p->tw, 0,
+                                             p->rows_total, p->P, p->c_pad, side->st);
+      if (e != cudaSuccess) return cuda_fail(e, "input transform");
+      e = cudaEventRecord(side->join, side->st);
+      if (e != cudaSuccess) return cuda_fail(e, "input transform join");
+    }
     cudaError_t e = launch_filter_transform(p->m, p->prec, g, ws, p->L.K, p->L.C, p->c_pad,
-                                            side ? side->st : s);
+                                            (side && !in_side) ? side->st : s);
     if (e != cudaSuccess) return cuda_fail(e, "filter transform");
-    if (side) {
+    if (side && !in_side) {
       e = cudaEventRecord(side->join, side->st);
       if (e != cudaSuccess) return cuda_fail(e, "filter transform join");
       filt_side = true;
     }
+    if (in_side) filt_side = true;  // the GEMM joins the side stream (now the input transform)
     tm.mark(0);
     U = ws;
     ws += p->u_bytes;
@@ -671,9 +688,12 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
     cudaStream_t cs = bi == 0 ? s : bi == 1 ? side->st : side->st2;
     unsigned char* V = ws + bi * vm;
     unsigned char* Mb = V + p->v_bytes;
-    cudaError_t e = launch_input_transform(p->m, p->prec, d, V, L.N, L.C, L.H, L.W, L.pad, p->th,
-                                           p->tw, row0, rows, Pc, p->c_pad, cs);
-    if (e != cudaSuccess) return cuda_fail(e, "input transform");
+    cudaError_t e = cudaSuccess;
+    if (!(in_side && ch == 0)) {  // (in_side: already enqueued on the side stream)
+      e = launch_input_transform(p->m, p->prec, d, V, L.N, L.C, L.H, L.W, L.pad, p->th, p->tw,
+                                 row0, rows, Pc, p->c_pad, cs);
+      if (e != cudaSuccess) return cuda_fail(e, "input transform");
+    }
     tm.mark(1);
     GemmArgs ga{V, U, Mb, p->a2, L.K, L.C, p->c_pad, Pc, p->bn, p->splits, p->m_ld, p->m_bf16};
     if (!odd) {
