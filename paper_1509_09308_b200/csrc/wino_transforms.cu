@@ -61,10 +61,9 @@ template <int M, typename TA>
 __device__ __forceinline__ void store_tile(TA* dst, int ow, int vr, int vc, const TA (&out)[M][M]);
 
 // ============================================================ filter transform
-// Block = 256 x FPT consecutive (k, c) pairs = contiguous 3x3 filters, staged
-// through shared memory with coalesced 16-byte loads (all of a thread's loads
-// in flight at once; the 36-byte records would otherwise give strided warp
-// loads), then thread t forms G g G^T for pairs t, t+256, ... and writes
+// Block = 256 x FPT consecutive (k, c) pairs = contiguous 3x3 filters, staged through shared memory with coalesced 16-byte loads (all
+// of a thread's loads in flight at once; the 36-byte records would otherwise
+// give strided warp loads), then thread t forms G g G^T for pairs t, t+256, ... and writes
 // U[s][comp][k][c] with c fastest (coalesced across the warp).
 // (engine.py:104-114)
 template <int M, int PREC, int FPT>
@@ -84,12 +83,19 @@ __global__ void __launch_bounds__(256) filter_transform_kernel(
   const T* src = g + t0 * 9;
   constexpr int VE = 16 / sizeof(T);  // elements per 16-byte load
   if (nloc == NP && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-    constexpr int NV = NP * 9 / VE / 256;  // 16-byte loads per thread
+    constexpr int NVT = NP * 9 / VE;           // 16-byte chunks in the block (NP % 4 == 0)
+    constexpr int NV = (NVT + 255) / 256;      // per thread, all in flight
     uint4 v[NV];
 #pragma unroll
-    for (int q = 0; q < NV; ++q) v[q] = __ldg(reinterpret_cast<const uint4*>(src) + threadIdx.x + 256 * q);
+    for (int q = 0; q < NV; ++q) {
+      const int i = threadIdx.x + 256 * q;
+      if (NVT % 256 == 0 || i < NVT) v[q] = __ldg(reinterpret_cast<const uint4*>(src) + i);
+    }
 #pragma unroll
-    for (int q = 0; q < NV; ++q) reinterpret_cast<uint4*>(sg)[threadIdx.x + 256 * q] = v[q];
+    for (int q = 0; q < NV; ++q) {
+      const int i = threadIdx.x + 256 * q;
+      if (NVT % 256 == 0 || i < NVT) reinterpret_cast<uint4*>(sg)[i] = v[q];
+    }
   } else {
     for (int e = threadIdx.x; e < nloc * 9; e += 256) sg[e] = __ldg(src + e);
   }
@@ -563,15 +569,23 @@ template <int M, int PREC>
 static void filter_launch(const void* g, void* U, int K, int C, int c_pad, cudaStream_t s) {
   using T = typename OpStore<PREC>::T;
   const long long n = static_cast<long long>(K) * C;
-  constexpr int FPT = sizeof(T) == 4 ? 4 : 2;  // 36 KB of staged filters per block
-  auto kern = filter_transform_kernel<M, PREC, FPT>;
-  static bool configured = false;
-  if (!configured) {
+  static const int fpt_env = getenv("WINO_FILTER_FPT") ? atoi(getenv("WINO_FILTER_FPT")) : 0;
+  // Four (k,c) per thread (two for fp64).  Alone on the GPU one per thread is
+  // twice as fast (512 x 512 F2 fp32: 4.1 vs 8.3 us), but in the pass the
+  // transform runs beside the input transform or just ahead of the GEMM, whose
+  // CTAs launch early (PDL) and co-reside only while the transform leaves SMs
+  // free: VGG-E F2 fp32 N=1 0.380 ms at four per thread vs 0.397 at one.
+  const int fpt = fpt_env == 1 || fpt_env == 2 || fpt_env == 4 ? fpt_env
+                                                               : (sizeof(T) == 4 ? 4 : 2);
+  auto go = [&](auto kern, int FPT) {
     max_carveout(kern);
-    configured = true;
-  }
-  launch_k(kern, dim3(static_cast<unsigned>((n + 256 * FPT - 1) / (256 * FPT))), dim3(256), 0, s,
-           static_cast<const T*>(g), U, K, C, c_pad);
+    launch_k(kern, dim3(static_cast<unsigned>((n + 256 * FPT - 1) / (256 * FPT))), dim3(256), 0, s,
+             static_cast<const T*>(g), U, K, C, c_pad);
+  };
+  if (fpt == 1) go(filter_transform_kernel<M, PREC, 1>, 1);
+  else if (fpt == 2) go(filter_transform_kernel<M, PREC, 2>, 2);
+  else if constexpr (sizeof(T) == 4) go(filter_transform_kernel<M, PREC, 4>, 4);
+  else go(filter_transform_kernel<M, PREC, 2>, 2);
 }
 
 template <int M>
