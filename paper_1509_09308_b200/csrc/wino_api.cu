@@ -34,6 +34,8 @@ struct wino_plan_s {
   int m_bf16;                        // M staged as bf16 (bf16 GEMM, staged, no split-C)
   int m_es;                          // M element bytes
   size_t u_bytes, v_bytes, m_bytes;  // v/m per full chunk
+  int u_split2;                      // non-FX 3xTF32 staged: U as hi/lo planes in the workspace
+  size_t u_ws;                       // workspace bytes of a forward-computed U
 };
 
 namespace wino {
@@ -419,6 +421,15 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
   }
   p->m_bf16 = (p->m_es == 2 && p->splits == 1 && !p->smallc && p->path == kPathStaged) ? 1 : 0;
   if (!p->m_bf16) p->m_es = p->acc_bytes;
+  // Non-FX 3xTF32 staged plans: the filter transform writes U as hi / lo planes
+  // in the workspace, so the GEMM's split warps only split V (into TMEM).
+  // Worth it when U is re-read by many tile blocks; with few (the small-P deep
+  // layers at N = 1) the doubled U write sits on the critical path instead
+  // (VGG-E N=1: 0.383 -> 0.397 ms if always on; N=64: 11.6 -> 11.2 ms).
+  p->u_split2 = (prec == kFP32 && p->path == kPathStaged && !p->smallc &&
+                 gemm_tmem_a_enabled() && (p->P + 127) / 128 >= 16 &&
+                 getenv("WINO_NO_USPLIT") == nullptr) ? 1 : 0;
+  p->u_ws = p->u_split2 ? 2 * p->u_bytes : p->u_bytes;
   p->m_bytes = (p->smallc || p->path != kPathStaged) ? 0
                         : align_up(static_cast<size_t>(p->splits) * p->a2 * L.K * p->m_ld *
                                        p->m_es,
@@ -457,7 +468,7 @@ int wino_plan_get_info(wino_plan_t p, wino_plan_info_t* info) {
   info->chunk_tiles = p->chunk_tiles;
   info->u_bytes = p->u_bytes;
   info->workspace_bytes =
-      p->u_bytes + p->nbuf * (p->v_bytes + p->m_bytes) + p->ypart_bytes;
+      p->u_ws + p->nbuf * (p->v_bytes + p->m_bytes) + p->ypart_bytes;
   info->launches_per_forward =
       p->smallc ? 1
                 : p->path == kPathFused  ? 1 + (p->fsplits > 1)
@@ -564,7 +575,7 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
   StageTimer tm(s, timer);
   unsigned char* ws = static_cast<unsigned char*>(workspace);
   size_t need =
-      p->nbuf * (p->v_bytes + p->m_bytes) + p->ypart_bytes + (U ? 0 : p->u_bytes);
+      p->nbuf * (p->v_bytes + p->m_bytes) + p->ypart_bytes + (U ? 0 : p->u_ws);
   if (workspace_bytes < need) {
     set_error("workspace too small: %zu < %zu bytes", workspace_bytes, need);
     return WINO_EINVAL;
@@ -590,11 +601,12 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
   // in-stream, so the GEMM launches programmatically (PDL) behind the longer of
   // the two instead of behind an event join.
   bool in_side = false;
+  const bool u_split = !U && p->u_split2;  // U computed here as hi / lo planes
   if (!U) {
     in_side = side && p->path == kPathStaged && p->num_chunks == 1 && !chunk_overlap &&
               static_cast<long long>(p->L.K) > p->P;
     if (in_side) {
-      cudaError_t e = launch_input_transform(p->m, p->prec, d, ws + p->u_bytes, p->L.N, p->L.C,
+      cudaError_t e = launch_input_transform(p->m, p->prec, d, ws + p->u_ws, p->L.N, p->L.C,
                                              p->L.H, p->L.W, p->L.pad, p->th, p->tw, 0,
                                              p->rows_total, p->P, p->c_pad, side->st);
       if (e != cudaSuccess) return cuda_fail(e, "input transform");
@@ -602,7 +614,7 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
       if (e != cudaSuccess) return cuda_fail(e, "input transform join");
     }
     cudaError_t e = launch_filter_transform(p->m, p->prec, g, ws, p->L.K, p->L.C, p->c_pad,
-                                            (side && !in_side) ? side->st : s);
+                                            (side && !in_side) ? side->st : s, u_split);
     if (e != cudaSuccess) return cuda_fail(e, "filter transform");
     if (side && !in_side) {
       e = cudaEventRecord(side->join, side->st);
@@ -612,7 +624,7 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
     if (in_side) filt_side = true;  // the GEMM joins the side stream (now the input transform)
     tm.mark(0);
     U = ws;
-    ws += p->u_bytes;
+    ws += p->u_ws;
   }
   int nstreams = (chunk_overlap && side) ? p->nbuf : 1;
   if (nstreams == 3) {  // third chunk stream: after the caller's prior work and U
@@ -695,7 +707,8 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
       if (e != cudaSuccess) return cuda_fail(e, "input transform");
     }
     tm.mark(1);
-    GemmArgs ga{V, U, Mb, p->a2, L.K, L.C, p->c_pad, Pc, p->bn, p->splits, p->m_ld, p->m_bf16};
+    GemmArgs ga{V, U, Mb, p->a2, L.K, L.C, p->c_pad, Pc, p->bn, p->splits, p->m_ld, p->m_bf16,
+                u_split ? 1 : 0};
     if (!odd) {
       e = join_filters();
       if (e != cudaSuccess) return cuda_fail(e, "filter transform join");

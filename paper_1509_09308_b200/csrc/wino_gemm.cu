@@ -97,7 +97,9 @@ __device__ __forceinline__ void split_region(uint32_t hi, int n, int lo_off, int
 // the MMAs of unit j+1.  Split-C units (small-P layers) write partial sums to
 // separate M slices that the output transform adds in a fixed order.
 // MB: store M as bf16 (the bf16 GEMM's staged M, wino_api.cu planner).
-template <int PREC, int BN, bool TA, bool MB>
+// BS (with TA): U arrives as hi / lo planes (filter transform split2), so the
+// B operand needs no on-chip split; TMA loads both planes into the stage.
+template <int PREC, int BN, bool TA, bool MB, bool BS = false>
 __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
     wgemm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmU,
                     const __grid_constant__ CUtensorMap tmM, int a2, int num_kb,
@@ -170,10 +172,13 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
           unsigned char* st = smem + s * Sm::stage_bytes;
           // HBM holds one plane; 3xTF32's lo planes are produced on chip
           if (dbg & 2) { ptx::mbar_arrive(&full[s]); continue; }
-          ptx::mbar_arrive_expect_tx(&full[s], Sm::a_bytes + Sm::b_bytes);
+          ptx::mbar_arrive_expect_tx(&full[s], Sm::a_bytes + (BS ? 2 : 1) * Sm::b_bytes);
           ptx::tma_load_3d(st, &tmV, &full[s], kb * Tr::bk, pb * kTileP, comp);
           ptx::tma_load_3d(st + (TA ? 1 : Tr::nsplit) * Sm::a_bytes, &tmU, &full[s], kb * Tr::bk, kbk * BN,
                            comp);
+          if constexpr (BS)  // lo plane of U right after the hi tile
+            ptx::tma_load_3d(st + Sm::a_bytes + Sm::b_bytes, &tmU, &full[s], kb * Tr::bk,
+                             kbk * BN, a2 + comp);
         }
       }
     }
@@ -249,7 +254,7 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
           ptx::mbar_wait(&full[s], (it / STAGES) & 1);
           const uint32_t st = ptx::smem_u32(smem + s * Sm::stage_bytes);
           if constexpr (TA) {
-            if (warp < 6 + 4) {
+            if (warp < 6 + 4 && !(dbg & 32)) {
               // A: thread = tile row r of its warp's TMEM lane quarter; the
               // 128-byte row (32 channels, 128B-swizzled) -> hi / lo columns
               const int q = warp & 3, r = 32 * q + lane;
@@ -276,7 +281,7 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
               ptx::tmem_st_32x32b_x32(t0 + 32, lo);
               ptx::tmem_st_wait();
               ptx::tc_fence_before();
-            } else if (!(dbg & 4)) {  // B: hi in place, lo plane, by the other 4 warps
+            } else if (!BS && warp >= 6 + 4 && !(dbg & 4)) {  // B: hi in place, lo plane, by the other 4 warps
               split_region_n<128>(st + Sm::a_bytes, Sm::b_bytes / 16, Sm::b_bytes, tid - 128);
             }
           } else if (!(dbg & 4)) {
@@ -426,23 +431,25 @@ static int num_sms() {
 }
 
 static int gemm_dbg() {  // diagnostic: 1 = skip M stores, 2 = skip operand loads,
-                         // 4 = skip the 3xTF32 split, 8 = skip the MMAs
+                         // 4 = skip the 3xTF32 (B) split, 8 = skip the MMAs,
+                         // 32 = skip the TMEM-A split
   static int v = -1;
   if (v < 0) v = getenv("WINO_GEMM_DBG") ? atoi(getenv("WINO_GEMM_DBG")) : 0;
   return v;
 }
 
-template <int PREC, int BN, bool TA, bool MB = false>
+template <int PREC, int BN, bool TA, bool MB = false, bool BS = false>
 static cudaError_t launch_tc(const GemmArgs& a, cudaStream_t s) {
   using Tr = GemmTraits<PREC>;
   using Sm = GemmSmem<PREC, BN, TA>;
   alignas(64) CUtensorMap tmV, tmU;
   const uint64_t es = Tr::esize;
   const uint64_t planes = static_cast<uint64_t>(op_splits(PREC)) * a.a2;  // planes in HBM
+  const uint64_t u_planes = BS ? 2 * planes : planes;
   if (!encode_tmap_3d(&tmV, PREC, a.V, a.C, a.Pc, planes, a.c_pad * es, a.Pc * a.c_pad * es,
                       Tr::bk, kTileP))
     return cudaErrorInvalidValue;
-  if (!encode_tmap_3d(&tmU, PREC, a.U, a.C, a.K, planes, a.c_pad * es,
+  if (!encode_tmap_3d(&tmU, PREC, a.U, a.C, a.K, u_planes, a.c_pad * es,
                       static_cast<uint64_t>(a.K) * a.c_pad * es, Tr::bk, BN))
     return cudaErrorInvalidValue;
   const int splits = a.splits < 1 ? 1 : a.splits;
@@ -451,7 +458,7 @@ static cudaError_t launch_tc(const GemmArgs& a, cudaStream_t s) {
   if (!encode_tmap_3d(&tmM, MB ? -2 : -1, a.M, a.Pc, a.K, static_cast<uint64_t>(splits) * a.a2,
                       a.m_ld * mes, static_cast<uint64_t>(a.K) * a.m_ld * mes, 32, 32))
     return cudaErrorInvalidValue;
-  auto kern = wgemm_tc_kernel<PREC, BN, TA, MB>;
+  auto kern = wgemm_tc_kernel<PREC, BN, TA, MB, BS>;
   static bool configured = false;  // idempotent attribute set
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -480,10 +487,21 @@ int gemm_num_kblocks(int prec, int C) {
 
 int gemm_device_sms() { return num_sms(); }
 
+bool gemm_tmem_a_enabled() { return getenv("WINO_NO_TMEM_A") == nullptr; }
+
 template <int PREC>
 static cudaError_t launch_prec(const GemmArgs& a, cudaStream_t s) {
   if constexpr (PREC == kFP32) {  // 3xTF32: A operand through tensor memory (BN <= 128)
     static const bool tmem_a = getenv("WINO_NO_TMEM_A") == nullptr;
+    if (tmem_a && a.b_split) {
+      switch (a.bn) {
+        case 32: return launch_tc<PREC, 32, true, false, true>(a, s);
+        case 64: return launch_tc<PREC, 64, true, false, true>(a, s);
+        case 128: return launch_tc<PREC, 128, true, false, true>(a, s);
+        default: return cudaErrorInvalidValue;
+      }
+    }
+    if (a.b_split) return cudaErrorInvalidValue;  // split planes need the TMEM-A kernel
     if (tmem_a) {
       switch (a.bn) {
         case 32: return launch_tc<PREC, 32, true>(a, s);

@@ -36,8 +36,10 @@ inline int op_splits(int) { return 1; }
 // All return cudaError_t of the launch.
 
 // g (K,C,3,3) [float or double] -> U [nsplit][alpha^2][K][c_pad]
+// split2 (FP32 only): write hi = rna_tf32(u) and lo = u - hi as two planes
+// (the staged 3xTF32 GEMM then needs no on-chip split of U).
 cudaError_t launch_filter_transform(int m, int prec, const void* g, void* U, int K, int C,
-                                    int c_pad, cudaStream_t s);
+                                    int c_pad, cudaStream_t s, bool split2 = false);
 
 // d (N,C,H,W) -> V [nsplit][alpha^2][Pc][c_pad] for tile rows [row0, row0+rows)
 cudaError_t launch_input_transform(int m, int prec, const void* d, void* V, int N, int C, int H,
@@ -80,9 +82,11 @@ struct GemmArgs {
   int splits;      // split-C factor: partial sums go to M slices [splits][a2][K][m_ld]
   long long m_ld;  // M row stride (>= Pc, multiple of 4 -- 8 for bf16 M -- for the TMA store)
   int m_bf16 = 0;  // bf16 GEMM only: M staged as bf16 (see wino_api.cu planner)
+  int b_split = 0; // 3xTF32 only: U holds [hi planes][lo planes] (no on-chip B split)
 };
 int gemm_num_kblocks(int prec, int C);
 int gemm_device_sms();
+bool gemm_tmem_a_enabled();  // 3xTF32 A operand through TMEM (WINO_NO_TMEM_A=1 disables)
 // Tensor-core (tcgen05) GEMM for FP32/TF32/BF16/FP16, CUDA-core fp64 for FP64.
 cudaError_t launch_batched_gemm(int prec, const GemmArgs& a, cudaStream_t s);
 int gemm_kernels_per_launch(int prec);

@@ -66,7 +66,7 @@ __device__ __forceinline__ void store_tile(TA* dst, int ow, int vr, int vc, cons
 // give strided warp loads), then thread t forms G g G^T for pairs t, t+256, ... and writes
 // U[s][comp][k][c] with c fastest (coalesced across the warp).
 // (engine.py:104-114)
-template <int M, int PREC, int FPT>
+template <int M, int PREC, int FPT, bool SPLIT2 = false>
 __global__ void __launch_bounds__(256) filter_transform_kernel(
     const typename OpStore<PREC>::T* __restrict__ g, void* __restrict__ U, int K, int C,
     int c_pad) {
@@ -121,7 +121,14 @@ __global__ void __launch_bounds__(256) filter_transform_kernel(
     for (int xi = 0; xi < AL; ++xi)
 #pragma unroll
       for (int nu = 0; nu < AL; ++nu) {
-        OpStore<PREC>::put(U, idx, plane, out[xi][nu]);
+        if constexpr (SPLIT2) {  // 3xTF32 hi / lo planes
+          uint32_t h;
+          asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(out[xi][nu]));
+          static_cast<float*>(U)[idx] = __uint_as_float(h);
+          static_cast<float*>(U)[idx + plane] = out[xi][nu] - __uint_as_float(h);
+        } else {
+          OpStore<PREC>::put(U, idx, plane, out[xi][nu]);
+        }
         idx += cstride;
       }
   }
@@ -566,7 +573,8 @@ static void max_carveout(F kern) {
 }
 
 template <int M, int PREC>
-static void filter_launch(const void* g, void* U, int K, int C, int c_pad, cudaStream_t s) {
+static void filter_launch(const void* g, void* U, int K, int C, int c_pad, cudaStream_t s,
+                          bool split2) {
   using T = typename OpStore<PREC>::T;
   const long long n = static_cast<long long>(K) * C;
   static const int fpt_env = getenv("WINO_FILTER_FPT") ? atoi(getenv("WINO_FILTER_FPT")) : 0;
@@ -582,6 +590,12 @@ static void filter_launch(const void* g, void* U, int K, int C, int c_pad, cudaS
     launch_k(kern, dim3(static_cast<unsigned>((n + 256 * FPT - 1) / (256 * FPT))), dim3(256), 0, s,
              static_cast<const T*>(g), U, K, C, c_pad);
   };
+  if constexpr (PREC == kFP32) {
+    if (split2) {
+      go(filter_transform_kernel<M, PREC, 4, true>, 4);
+      return;
+    }
+  }
   if (fpt == 1) go(filter_transform_kernel<M, PREC, 1>, 1);
   else if (fpt == 2) go(filter_transform_kernel<M, PREC, 2>, 2);
   else if constexpr (sizeof(T) == 4) go(filter_transform_kernel<M, PREC, 4>, 4);
@@ -590,23 +604,23 @@ static void filter_launch(const void* g, void* U, int K, int C, int c_pad, cudaS
 
 template <int M>
 static cudaError_t filter_dispatch(int prec, const void* g, void* U, int K, int C, int c_pad,
-                                   cudaStream_t s) {
+                                   cudaStream_t s, bool split2) {
   switch (prec) {
-    case kFP32: filter_launch<M, kFP32>(g, U, K, C, c_pad, s); break;
-    case kTF32: filter_launch<M, kTF32>(g, U, K, C, c_pad, s); break;
-    case kBF16: filter_launch<M, kBF16>(g, U, K, C, c_pad, s); break;
-    case kFP16: filter_launch<M, kFP16>(g, U, K, C, c_pad, s); break;
-    case kFP64: filter_launch<M, kFP64>(g, U, K, C, c_pad, s); break;
+    case kFP32: filter_launch<M, kFP32>(g, U, K, C, c_pad, s, split2); break;
+    case kTF32: filter_launch<M, kTF32>(g, U, K, C, c_pad, s, false); break;
+    case kBF16: filter_launch<M, kBF16>(g, U, K, C, c_pad, s, false); break;
+    case kFP16: filter_launch<M, kFP16>(g, U, K, C, c_pad, s, false); break;
+    case kFP64: filter_launch<M, kFP64>(g, U, K, C, c_pad, s, false); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
 }
 
 cudaError_t launch_filter_transform(int m, int prec, const void* g, void* U, int K, int C,
-                                    int c_pad, cudaStream_t s) {
+                                    int c_pad, cudaStream_t s, bool split2) {
   if (K <= 0 || C <= 0) return cudaSuccess;
-  return m == 2 ? filter_dispatch<2>(prec, g, U, K, C, c_pad, s)
-                : filter_dispatch<4>(prec, g, U, K, C, c_pad, s);
+  return m == 2 ? filter_dispatch<2>(prec, g, U, K, C, c_pad, s, split2)
+                : filter_dispatch<4>(prec, g, U, K, C, c_pad, s, split2);
 }
 
 // ------------------------------------------------ TMA-staged input transform

@@ -309,3 +309,26 @@ def test_bf16_staged_m_error_budget(wb, monkeypatch, m):
     assert np.abs(e16).max() / scale <= REL_TOL[("bf16", m)]
     rms16, rms32 = np.sqrt((e16 ** 2).mean()), np.sqrt((e32 ** 2).mean())
     assert rms16 <= 1.35 * rms32, (rms16, rms32)
+
+
+def test_presplit_filter_planes_bitwise(wb, monkeypatch):
+    """Non-FX 3xTF32 plans with many tile blocks get U from the filter transform
+    as hi / lo planes (no on-chip split of U in the GEMM); FX plans pass a
+    one-plane U that the GEMM splits on chip.  Both feed the MMAs the same
+    rna_tf32 hi and exact lo, so the outputs are bit-identical -- and within
+    the fp32 gates of the oracle."""
+    import torch
+    monkeypatch.setenv("WINO_PATH", "staged")
+    cfg = wb.LayerConfig(N=4, C=64, H=64, W=64, K=64, pad=1)
+    dn = O.fill_uniform((4, 64, 64, 64), 71)
+    gn = O.fill_uniform((64, 64, 3, 3), 72)
+    d, g = torch.from_numpy(dn).cuda(), torch.from_numpy(gn).cuda()
+    plan = wb.WinogradPlan(cfg, 2, "fp32")
+    y_nonfx = plan.forward(d, g=g)
+    y_fx = plan.forward(d, U=plan.filter_transform(g))
+    torch.cuda.synchronize()
+    assert torch.equal(y_nonfx, y_fx)
+    y = y_nonfx.cpu().numpy()
+    assert O.max_abs_error(y, O.direct_forward(dn, gn, 1)) < 5e-4
+    yo = O.winograd_forward(dn, gn, 2, 1)
+    assert np.abs(y - yo).max() <= 2e-5 * (1 + np.abs(yo).max())
