@@ -696,7 +696,7 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
     // serialises chunks that share a buffer; U precedes on `side`, and the
     // third stream waited for it at the fork)
     const int bi = (chunk_overlap && side) ? ch % nstreams : 0;
-    const bool odd = bi != 0;
+    const bool side_chunk = bi != 0;  // U reached its stream at the fork / in order
     cudaStream_t cs = bi == 0 ? s : bi == 1 ? side->st : side->st2;
     unsigned char* V = ws + bi * vm;
     unsigned char* Mb = V + p->v_bytes;
@@ -709,7 +709,7 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
     tm.mark(1);
     GemmArgs ga{V, U, Mb, p->a2, L.K, L.C, p->c_pad, Pc, p->bn, p->splits, p->m_ld, p->m_bf16,
                 u_split ? 1 : 0};
-    if (!odd) {
+    if (!side_chunk) {
       e = join_filters();
       if (e != cudaSuccess) return cuda_fail(e, "filter transform join");
     }
