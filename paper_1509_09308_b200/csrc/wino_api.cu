@@ -30,7 +30,7 @@ struct wino_plan_s {
   size_t ypart_bytes;
   int rows_total, rows_per_chunk, num_chunks;
   long long chunk_tiles;
-  long long m_ld;                    // M row stride (tiles, multiple of 4; 8 for bf16 M)
+  long long m_ld;                    // M row stride (tiles, multiple of 64: 128-byte rows)
   int m_bf16;                        // M staged as bf16 (bf16 GEMM, staged, no split-C)
   int m_es;                          // M element bytes
   size_t u_bytes, v_bytes, m_bytes;  // v/m per full chunk
@@ -341,7 +341,7 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
     p->chunk_tiles = p->P;
     p->splits = 1;
   }
-  p->m_ld = static_cast<long long>(align_up(static_cast<size_t>(p->chunk_tiles), 8));
+  p->m_ld = static_cast<long long>(align_up(static_cast<size_t>(p->chunk_tiles), 64));
   // ---- path (WINO_PATH=staged|fused|hybrid overrides the choice; read at
   // plan creation):
   //   staged : input transform -> GEMM -> output transform, V and M staged;
@@ -415,7 +415,7 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
     p->v_bytes = align_up(static_cast<size_t>(p->nsplit) * p->a2 * p->chunk_tiles * p->c_pad *
                               p->esize,
                           1024);
-    p->m_ld = static_cast<long long>(align_up(static_cast<size_t>(p->chunk_tiles), 8));
+    p->m_ld = static_cast<long long>(align_up(static_cast<size_t>(p->chunk_tiles), 64));
     p->overlap = p->num_chunks > 1;
     if (!p->overlap) p->nbuf = 1;
   }

@@ -471,7 +471,7 @@ struct OutTma {
 template <int M, typename MT>
 __global__ void __launch_bounds__(kOutTP) output_transform_tma_kernel(
     const __grid_constant__ CUtensorMap tmM, float* __restrict__ y, int K, int th, int tw, int oh,
-    int ow, int row0, long long Pc) {
+    int ow, int row0, long long Pc, const char* __restrict__ mbase, long long m_ld, int discard) {
   using A = Alg<M>;
   using Cfg = OutTma<M, MT>;
   constexpr int AL = A::alpha;
@@ -493,6 +493,24 @@ __global__ void __launch_bounds__(kOutTP) output_transform_tma_kernel(
     ptx::tma_load_3d(s, &tmM, &bar, p0, k0, 0);
   }
   ptx::mbar_wait(&bar, 0);
+  if (discard) {
+    // M is dead once this box is in smem: drop its (dirty) L2 lines so they are
+    // never written back to HBM.  Rows start 128-byte aligned (m_ld % 64 == 0);
+    // lines past the row's m_ld belong to the next row and are left alone.
+    constexpr int EPL = 128 / static_cast<int>(sizeof(MT));  // elements per line
+    constexpr int LPR = kOutTP / EPL;                         // lines per box row
+    constexpr int NL = Cfg::alpha * Cfg::alpha * Cfg::OF * LPR;
+    for (int i = threadIdx.x; i < NL; i += kOutTP) {
+      const int row = i / LPR, l = i - (i / LPR) * LPR;
+      const int comp = row / Cfg::OF, k = k0 + (row - comp * Cfg::OF);
+      const long long e0 = static_cast<long long>(p0) + l * EPL;
+      if (k < K && e0 < m_ld) {
+        const char* a = mbase + ((static_cast<long long>(comp) * K + k) * m_ld + e0) *
+                                    static_cast<long long>(sizeof(MT));
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
+      }
+    }
+  }
   const int t = threadIdx.x;
   const long long p = static_cast<long long>(p0) + t;
   if (p >= Pc) return;
@@ -856,8 +874,11 @@ static cudaError_t output_tma_launch(const void* Mbuf, void* y, int K, int th, i
     configured = true;
   }
   const dim3 grid(static_cast<unsigned>((Pc + kOutTP - 1) / kOutTP), (K + Cfg::OF - 1) / Cfg::OF);
+  static const bool no_discard = getenv("WINO_NO_DISCARD") != nullptr;
+  const int discard = !no_discard && m_ld % 64 == 0 && (reinterpret_cast<uintptr_t>(Mbuf) & 127) == 0;
   launch_k(kern, grid, dim3(kOutTP), static_cast<size_t>(Cfg::bytes + 128), s, tmM,
-           static_cast<float*>(y), K, th, tw, oh, ow, row0, Pc);
+           static_cast<float*>(y), K, th, tw, oh, ow, row0, Pc,
+           static_cast<const char*>(Mbuf), m_ld, discard);
   return cudaGetLastError();
 }
 
