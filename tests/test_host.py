@@ -212,3 +212,24 @@ def test_report_text_and_csv():
     assert "conv1.1,f4x4,1,0.5,123.25" in r.to_csv()
     txt = r.to_text()
     assert "conv1.1" in txt and "123.2" in txt and "-" in txt.splitlines()[-1]
+
+
+def test_planner_decisions_vgg():
+    """The C planner's choices on VGG-E layers (plan creation needs no GPU):
+    split-C from the waves x k-steps cost model, bf16-staged M, two chunk
+    buffers for multi-chunk staged plans, pre-split U workspace for large P."""
+    import paper_1509_09308_b200 as wb
+
+    def info(C, H, K, m, prec, N):
+        return wb.WinogradPlan(wb.LayerConfig(N=N, C=C, H=H, W=H, K=K, pad=1), m, prec).info
+
+    conv5 = info(512, 14, 512, 2, "fp32", 1)      # 1 tile block x 4 x 16 = 64 units
+    assert conv5["gemm_splits"] == 2 and conv5["m_bytes_per_elem"] == 4
+    conv42 = info(512, 28, 512, 2, "fp32", 1)     # 128 units: one wave without a split
+    assert conv42["gemm_splits"] == 1
+    conv32 = info(256, 56, 256, 4, "bf16", 64)
+    assert conv32["m_bytes_per_elem"] == 2 and conv32["num_chunks"] > 1
+    conv12 = info(64, 224, 64, 2, "fp32", 64)
+    assert conv12["num_chunks"] > 1 and conv12["m_bytes_per_elem"] == 4
+    # large-P 3xTF32: workspace holds U as hi/lo planes (2 x u_bytes) + two V/M chunk sets
+    assert conv12["workspace_bytes"] >= 2 * conv12["u_bytes"]
