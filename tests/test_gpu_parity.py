@@ -332,3 +332,19 @@ def test_presplit_filter_planes_bitwise(wb, monkeypatch):
     assert O.max_abs_error(y, O.direct_forward(dn, gn, 1)) < 5e-4
     yo = O.winograd_forward(dn, gn, 2, 1)
     assert np.abs(y - yo).max() <= 2e-5 * (1 + np.abs(yo).max())
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp16"])
+def test_tma_input_odd_channels_16bit(wb, prec):
+    """TMA input transform with 16-bit operands and an odd channel count (a
+    partial second block of 32 channels: zero-filled box channels past C must
+    never be stored)."""
+    import torch
+    cfg = wb.LayerConfig(N=2, C=37, H=16, W=16, K=20, pad=1)
+    dn = O.fill_uniform((2, 37, 16, 16), 81)
+    gn = O.fill_uniform((20, 37, 3, 3), 82)
+    d, g = torch.from_numpy(dn).cuda(), torch.from_numpy(gn).cuda()
+    ref = O.direct_forward(dn, gn, 1)
+    for m in (2, 4):
+        y = wb.WinogradPlan(cfg, m, prec).forward(d, g=g).cpu().numpy()
+        assert O.max_abs_error(y, ref) / np.abs(ref).max() <= REL_TOL[(prec, m)], (m, prec)
