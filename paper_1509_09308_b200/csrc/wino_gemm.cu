@@ -362,6 +362,323 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
   }
 }
 
+// ------------------------------------------------------------ CTA-pair 3xTF32
+// cta_group::2 variant of the TMEM-A 3xTF32 GEMM: a cluster of two CTAs on one
+// TPC computes a 256-tile x BN-filter block per unit.  Each CTA stages its own
+// 128 tile rows (A, split into its own TMEM) and HALF of the filter block (B),
+// so each SM's shared memory carries half the B bytes, half the B split and
+// half the MMA's B reads of the single-CTA kernel.  The leader CTA issues
+// tcgen05.mma.cta_group::2 (M = 256); D rows 0-127 land in the leader's TMEM,
+// 128-255 in the peer's.  Synchronisation: each CTA waits on its own full
+// barrier; both CTAs' split warps arrive on the leader's sfull; the leader's
+// commits multicast to both CTAs' empty / tfull; both epilogues arrive on the
+// leader's tempty.
+template <int BN, bool BS>
+__global__ void __launch_bounds__(gemm_threads<kFP32>(), 1)
+    wgemm_tc2_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmU,
+                     const __grid_constant__ CUtensorMap tmM, int a2, int num_kb,
+                     int kb_per_split, int n_ppblk, int n_kblk, int n_units) {
+  using Tr = GemmTraits<kFP32>;
+  constexpr int HB = BN / 2;                 // filters staged per CTA
+  constexpr int a_bytes = kTileP * 128;
+  constexpr int b_bytes = HB * 128;
+  constexpr int stage_bytes = a_bytes + 2 * b_bytes;
+  constexpr int epi_bytes = kEpiWarps * 2 * kEpiBuf;
+  constexpr int avail = 227 * 1024 - 1024 - 512 - epi_bytes;
+  constexpr int STAGES = avail / stage_bytes >= 4 ? 4 : avail / stage_bytes;
+  static_assert(2 * BN + 64 * STAGES <= 512, "TMEM budget");
+  constexpr int epi_offset = STAGES * stage_bytes;
+  constexpr int bar_offset = epi_offset + epi_bytes;
+  constexpr int a_tmem_col = 2 * BN;
+
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + bar_offset);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* sfull = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sfull + STAGES);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmV);
+    ptx::prefetch_tmap(&tmU);
+    ptx::prefetch_tmap(&tmM);
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&sfull[s], 2 * kSplitWarps);  // both CTAs' split warps (leader's copy used)
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&tfull[b], 1);
+      ptx::mbar_init(&tempty[b], 256);  // both CTAs' epilogue threads (leader's copy used)
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     ptx::smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  griddep_launch();
+  griddep_wait();
+
+  auto decode = [&](int u, int& pp, int& kbk, int& comp, int& split) {
+    pp = u % n_ppblk;
+    int r = u / n_ppblk;
+    kbk = r % n_kblk;
+    r /= n_kblk;
+    comp = r % a2;
+    split = r / a2;
+  };
+  const uint32_t mask2 = 3u;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- producer: own A rows, own half of B
+      int it = 0;
+      for (int u = cid; u < n_units; u += ncl) {
+        int pp, kbk, comp, split;
+        decode(u, pp, kbk, comp, split);
+        const int kb0 = split * kb_per_split;
+        const int kb1 = min(num_kb, kb0 + kb_per_split);
+        const int prow = (2 * pp + static_cast<int>(rank)) * kTileP;
+        const int frow = kbk * BN + static_cast<int>(rank) * HB;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % STAGES;
+          ptx::mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+          unsigned char* st = smem + s * stage_bytes;
+          ptx::mbar_arrive_expect_tx(&full[s], a_bytes + (BS ? 2 : 1) * b_bytes);
+          ptx::tma_load_3d(st, &tmV, &full[s], kb * Tr::bk, prow, comp);
+          ptx::tma_load_3d(st + a_bytes, &tmU, &full[s], kb * Tr::bk, frow, comp);
+          if constexpr (BS)
+            ptx::tma_load_3d(st + a_bytes + b_bytes, &tmU, &full[s], kb * Tr::bk, frow, a2 + comp);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {  // ---- MMA issuer (leader only), M = 256
+      constexpr uint32_t idesc = ptx::umma_idesc(Tr::fmt, 2 * kTileP, BN);
+      int it = 0, j = 0;
+      for (int u = cid; u < n_units; u += ncl, ++j) {
+        int pp, kbk, comp, split;
+        decode(u, pp, kbk, comp, split);
+        const int kb0 = split * kb_per_split;
+        const int kb1 = min(num_kb, kb0 + kb_per_split);
+        const int acc = j & 1;
+        ptx::mbar_wait(&tempty[acc], ((j >> 1) & 1) ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % STAGES;
+          ptx::mbar_wait(&sfull[s], (it / STAGES) & 1);
+          ptx::tc_fence_after();
+          const uint32_t st = ptx::smem_u32(smem + s * stage_bytes);
+          const uint32_t b_hi = st + a_bytes, b_lo = b_hi + b_bytes;
+          const uint32_t ta_hi = tmem_base + a_tmem_col + 64 * s, ta_lo = ta_hi + 32;
+#pragma unroll
+          for (int k = 0; k < Tr::bk / Tr::uk; ++k) {
+            const uint32_t off = k * 32;
+            const uint32_t accum = (kb != kb0 || k != 0) ? 1u : 0u;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+                "r"(ta_lo + 8 * k), "l"(ptx::umma_desc_sw128(b_hi + off)), "r"(idesc), "r"(accum));
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+                "r"(ta_hi + 8 * k), "l"(ptx::umma_desc_sw128(b_lo + off)), "r"(idesc), "r"(1u));
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+                "r"(ta_hi + 8 * k), "l"(ptx::umma_desc_sw128(b_hi + off)), "r"(idesc), "r"(1u));
+          }
+          asm volatile(  // frees stage s in both CTAs
+              "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                  ptx::smem_u32(&empty[s])),
+              "h"(static_cast<unsigned short>(mask2))
+              : "memory");
+        }
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                ptx::smem_u32(&tfull[acc])),
+            "h"(static_cast<unsigned short>(mask2))
+            : "memory");
+      }
+    }
+  } else if (warp >= 6) {  // ---- split warps: A rows -> own TMEM, own B half in smem
+    const int tid = threadIdx.x - 192;
+    const uint32_t sfull_leader = ptx::mapa(ptx::smem_u32(sfull), 0);
+    int it = 0;
+    for (int u = cid; u < n_units; u += ncl) {
+      int pp, kbk, comp, split;
+      decode(u, pp, kbk, comp, split);
+      const int kb0 = split * kb_per_split;
+      const int kb1 = min(num_kb, kb0 + kb_per_split);
+      for (int kb = kb0; kb < kb1; ++kb, ++it) {
+        const int s = it % STAGES;
+        ptx::mbar_wait(&full[s], (it / STAGES) & 1);
+        const uint32_t st = ptx::smem_u32(smem + s * stage_bytes);
+        if (warp < 6 + 4) {
+          const int q = warp & 3, r = 32 * q + lane;
+          const uint32_t row = st + 128 * r;
+          uint32_t hi[32], lo[32];
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            float x0, x1, x2, x3;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(x0), "=f"(x1), "=f"(x2), "=f"(x3)
+                         : "r"(row + 16 * (jj ^ (r & 7))));
+            const float xs[4] = {x0, x1, x2, x3};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              uint32_t h;
+              asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(xs[e]));
+              hi[4 * jj + e] = h;
+              lo[4 * jj + e] = __float_as_uint(xs[e] - __uint_as_float(h));
+            }
+          }
+          const uint32_t t0 =
+              tmem_base + (static_cast<uint32_t>(32 * q) << 16) + a_tmem_col + 64 * s;
+          ptx::tmem_st_32x32b_x32(t0, hi);
+          ptx::tmem_st_32x32b_x32(t0 + 32, lo);
+          ptx::tmem_st_wait();
+          ptx::tc_fence_before();
+        } else if (!BS) {
+          split_region_n<128>(st + a_bytes, b_bytes / 16, b_bytes, tid - 128);
+        }
+        ptx::fence_async_smem();
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                           sfull_leader + 8 * s)
+                       : "memory");
+      }
+    }
+  } else {  // ---- epilogue: own TMEM rows = own 128 tiles
+    const int q = warp & 3;
+    float* buf0 = reinterpret_cast<float*>(smem + epi_offset + (warp - 2) * 2 * kEpiBuf);
+    const uint32_t sbuf0 = ptx::smem_u32(buf0) + 4 * lane;
+    const uint32_t tempty_leader = ptx::mapa(ptx::smem_u32(tempty), 0);
+    int j = 0, nbuf = 0;
+    for (int u = cid; u < n_units; u += ncl, ++j) {
+      int pp, kbk, comp, split;
+      decode(u, pp, kbk, comp, split);
+      const int acc = j & 1;
+      ptx::mbar_wait(&tfull[acc], (j >> 1) & 1);
+      ptx::tc_fence_after();
+      const int p0 = (2 * pp + static_cast<int>(rank)) * kTileP + q * 32;
+      const int z = split * a2 + comp;
+      const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+      constexpr int NC = BN / 32;
+      uint32_t r[2][32];
+      ptx::tmem_ld_32x32b_x32(taddr, r[0]);
+#pragma unroll
+      for (int ci = 0; ci < NC; ++ci) {
+        ptx::tmem_ld_wait();
+        if (ci + 1 < NC) {
+          ptx::tmem_ld_32x32b_x32(taddr + 32 * (ci + 1), r[(ci + 1) & 1]);
+        } else {
+          ptx::tc_fence_before();
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                           tempty_leader + 8 * acc)
+                       : "memory");
+        }
+        const int b = nbuf++ & 1;
+        if (lane == 0) ptx::bulk_wait_read<1>();
+        __syncwarp();
+        const uint32_t sb = sbuf0 + b * kEpiBuf;
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj)
+          asm volatile("st.shared.b32 [%0], %1;" ::"r"(sb + jj * 128), "r"(r[ci & 1][jj]) : "memory");
+        ptx::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          ptx::tma_store_3d(&tmM, buf0 + b * (kEpiBuf / 4), p0, kbk * BN + 32 * ci, z);
+          ptx::bulk_commit();
+        }
+      }
+    }
+    if (lane == 0) ptx::bulk_wait_all();
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  if (warp == 1) {
+    __syncwarp();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+  }
+}
+
+static int num_sms();
+
+template <int BN, bool BS>
+static cudaError_t launch_tc2(const GemmArgs& a, cudaStream_t s) {
+  using Tr = GemmTraits<kFP32>;
+  constexpr int HB = BN / 2;
+  constexpr int stage_bytes = kTileP * 128 + 2 * HB * 128;
+  constexpr int epi_bytes = kEpiWarps * 2 * kEpiBuf;
+  constexpr int avail = 227 * 1024 - 1024 - 512 - epi_bytes;
+  constexpr int STAGES = avail / stage_bytes >= 4 ? 4 : avail / stage_bytes;
+  constexpr int total = STAGES * stage_bytes + epi_bytes + 512 + 1024;
+  alignas(64) CUtensorMap tmV, tmU, tmM;
+  const uint64_t es = 4;
+  const uint64_t planes = static_cast<uint64_t>(a.a2);
+  if (!encode_tmap_3d(&tmV, kFP32, a.V, a.C, a.Pc, planes, a.c_pad * es, a.Pc * a.c_pad * es,
+                      Tr::bk, kTileP))
+    return cudaErrorInvalidValue;
+  if (!encode_tmap_3d(&tmU, kFP32, a.U, a.C, a.K, BS ? 2 * planes : planes, a.c_pad * es,
+                      static_cast<uint64_t>(a.K) * a.c_pad * es, Tr::bk, HB))
+    return cudaErrorInvalidValue;
+  const int splits = a.splits < 1 ? 1 : a.splits;
+  if (!encode_tmap_3d(&tmM, -1, a.M, a.Pc, a.K, static_cast<uint64_t>(splits) * a.a2, a.m_ld * 4ull,
+                      static_cast<uint64_t>(a.K) * a.m_ld * 4ull, 32, 32))
+    return cudaErrorInvalidValue;
+  auto kern = wgemm_tc2_kernel<BN, BS>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, total);
+    if (e != cudaSuccess) return e;
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    configured = true;
+  }
+  const int num_kb = (a.C + Tr::bk - 1) / Tr::bk;
+  const int kbps = (num_kb + splits - 1) / splits;
+  const int n_ppblk = static_cast<int>((a.Pc + 2 * kTileP - 1) / (2 * kTileP));
+  const int n_kblk = (a.K + BN - 1) / BN;
+  const long long units = static_cast<long long>(n_ppblk) * n_kblk * a.a2 * splits;
+  if (units > 0x7fffffffLL) return cudaErrorInvalidValue;
+  const int clusters = static_cast<int>(units < num_sms() / 2 ? units : num_sms() / 2);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * clusters);
+  cfg.blockDim = dim3(gemm_threads<kFP32>());
+  cfg.dynamicSmemBytes = total;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmV, tmU, tmM, a.a2, num_kb, kbps, n_ppblk,
+                                     n_kblk, static_cast<int>(units));
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------ fp64 CUDA-core
 // 64 x 64 output block, 16-channel smem slices, c-ascending accumulation
 // (deterministic, same reduction order as kernels.py:43-47).
@@ -493,6 +810,12 @@ template <int PREC>
 static cudaError_t launch_prec(const GemmArgs& a, cudaStream_t s) {
   if constexpr (PREC == kFP32) {  // 3xTF32: A operand through tensor memory (BN <= 128)
     static const bool tmem_a = getenv("WINO_NO_TMEM_A") == nullptr;
+    static const bool pair = getenv("WINO_GEMM_2SM") != nullptr;
+    if (tmem_a && pair && (a.bn == 64 || a.bn == 128)) {
+      if (a.b_split)
+        return a.bn == 64 ? launch_tc2<64, true>(a, s) : launch_tc2<128, true>(a, s);
+      return a.bn == 64 ? launch_tc2<64, false>(a, s) : launch_tc2<128, false>(a, s);
+    }
     if (tmem_a && a.b_split) {
       switch (a.bn) {
         case 32: return launch_tc<PREC, 32, true, false, true>(a, s);

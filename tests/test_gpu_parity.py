@@ -348,3 +348,19 @@ def test_tma_input_odd_channels_16bit(wb, prec):
     for m in (2, 4):
         y = wb.WinogradPlan(cfg, m, prec).forward(d, g=g).cpu().numpy()
         assert O.max_abs_error(y, ref) / np.abs(ref).max() <= REL_TOL[(prec, m)], (m, prec)
+
+
+def test_cta_pair_gemm_variant_parity():
+    """The cta_group::2 (CTA-pair) 3xTF32 GEMM variant, selected by
+    WINO_GEMM_2SM=1 at first use in a fresh process, passes the fp32 gates
+    (it is not the default: measured slower)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "tools", "gemm2sm_check.py")],
+                         env={**os.environ, "WINO_GEMM_2SM": "1"}, capture_output=True,
+                         text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("N=")]
+    assert len(lines) == 5 and all(l.endswith("OK") for l in lines), out.stdout
