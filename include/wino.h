@@ -135,6 +135,15 @@ int wino_grad_weights(const wino_layer_t* layer, int prec, const void* d, const 
                       void* dg, void* workspace, size_t workspace_bytes, size_t workspace_limit,
                       void* stream);
 
+/* Direct correlation with zero padding (any R x S), the reference's `direct` /
+ * `direct-fp32` algorithms and cmd_accuracy's fp64 oracle (direct.py:82-114):
+ * accumulation order c, v, u with a rounded multiply then a rounded add in the
+ * accumulator precision, so the output is bitwise the reference's.
+ * in_prec / acc_prec: WINO_PREC_FP32 or WINO_PREC_FP64 (d, g in in_prec; y in
+ * acc_prec).  Device pointers, enqueued on `stream`. */
+int wino_direct_forward(const wino_layer_t* layer, int in_prec, int acc_prec, const void* d,
+                        const void* g, void* y, void* stream);
+
 const char* wino_last_error(void);
 /* Library version string. */
 const char* wino_version(void);

@@ -7,7 +7,9 @@ computed by hand-written CUDA kernels in ``libwino.so`` (C ABI:
 fails loudly if it is missing: there is no CPU fallback.
 """
 from ._lib import version  # noqa: F401  (loads libwino.so or raises)
-from .commands import BENCH_ALGOS, cmd_bench, layer_inputs, parse_algo, run_layer
+from .commands import (ACCURACY_ALGOS, BENCH_ALGOS, cmd_accuracy, cmd_bench, layer_inputs,
+                       parse_algo, run_layer)
+from .direct import direct_forward
 from .engine import (FilterCache, TileGrid, WinogradPlan, get_plan, multiply_stage_flops,
                      shared_filter_cache, tile_count, winograd_forward, winograd_grad_inputs,
                      winograd_grad_weights, grad_weights_device)
@@ -22,6 +24,7 @@ __all__ = [
     "LayerConfig", "gflops_direct", "WinogradAlgorithm", "builtin", "builtin_sizes",
     "OpCounter", "FilterCache", "TileGrid", "tile_count", "multiply_stage_flops",
     "winograd_forward", "winograd_grad_inputs", "winograd_grad_weights", "grad_weights_device", "shared_filter_cache", "WinogradPlan",
-    "get_plan", "run_layer", "cmd_bench", "layer_inputs", "parse_algo", "BENCH_ALGOS",
+    "get_plan", "run_layer", "cmd_bench", "cmd_accuracy", "layer_inputs", "parse_algo",
+    "BENCH_ALGOS", "ACCURACY_ALGOS", "direct_forward",
     "LayerSuite", "get_suite", "vgg_e", "vgg_e_accuracy", "version", "__version__",
 ]

@@ -1,11 +1,12 @@
 """Command line for the GPU path: ``python -m paper_1509_09308_b200 bench ...``.
 
-Mirrors the ``bench`` command of the reference CLI (winoconv/cli.py:38-83,
-110-159): same flags (--suite --algo --batch --repeats --seed --scale --format
---out), same report (commands.cmd_bench, commands.py:136-178) and exit codes
-(0 ok, 1 usage / domain error, 2 runtime failure).  Algorithm names are the
-reference's Winograd names, optionally with a GEMM precision suffix
-(``f4x4-fx:bf16``).  The CLI runs in-process; there is no HTTP transport.
+Mirrors the ``bench`` and ``accuracy`` commands of the reference CLI
+(winoconv/cli.py:38-83, 110-159): same flags, same reports
+(commands.cmd_bench / cmd_accuracy, commands.py:64-178) and exit codes (0 ok,
+1 usage / domain error, 2 runtime failure).  Algorithm names are the
+reference's (Winograd names optionally with a GEMM precision suffix,
+``f4x4-fx:bf16``; ``fft`` is not on the GPU path).  The CLI runs in-process;
+there is no HTTP transport.
 """
 from __future__ import annotations
 
@@ -28,18 +29,31 @@ def build_parser() -> argparse.ArgumentParser:
     pb.add_argument("--format", choices=("csv", "text"), default="csv")
     pb.add_argument("--out", metavar="FILE", default=None,
                     help="write the report here instead of stdout")
+    pa = sub.add_parser("accuracy", help="max abs error vs the fp64 direct oracle (GPU)")
+    pa.add_argument("--suite", default="vgg-e-accuracy")
+    pa.add_argument("--algos", default="direct-fp32,f2x2,f4x4",
+                    help="comma-separated algorithm names")
+    pa.add_argument("--precision", choices=("fp32", "fp16"), default="fp32")
+    pa.add_argument("--seed", type=int, default=0)
+    pa.add_argument("--scale", type=float, default=1.0)
+    pa.add_argument("--format", choices=("csv", "text"), default="csv")
+    pa.add_argument("--out", metavar="FILE", default=None)
     return p
 
 
 def main(argv: Optional[list] = None) -> int:
     args = build_parser().parse_args(argv)
-    from .commands import cmd_bench, parse_algo
+    from .commands import cmd_accuracy, cmd_bench, parse_algo
     try:
-        parse_algo(args.algo)
-        if args.batch < 1:
-            raise ValueError(f"batch must be >= 1, got {args.batch}")
-        rep = cmd_bench(suite=args.suite, algo=args.algo, batch=args.batch,
-                        repeats=args.repeats, scale=args.scale, seed=args.seed)
+        if args.command == "accuracy":
+            rep = cmd_accuracy(suite=args.suite, algos=[a for a in args.algos.split(",") if a],
+                               precision=args.precision, seed=args.seed, scale=args.scale)
+        else:
+            parse_algo(args.algo)
+            if args.batch < 1:
+                raise ValueError(f"batch must be >= 1, got {args.batch}")
+            rep = cmd_bench(suite=args.suite, algo=args.algo, batch=args.batch,
+                            repeats=args.repeats, scale=args.scale, seed=args.seed)
     except (ValueError, KeyError) as e:
         sys.stderr.write(f"paper_1509_09308_b200: error: {e}\n")
         return 1

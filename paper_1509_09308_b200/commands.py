@@ -1,20 +1,25 @@
-"""Algorithm-name dispatch and the layer benchmark on the GPU path
-(mirrors winoconv/commands.py:25-178 for the Winograd algorithms).
+"""Algorithm-name dispatch, the accuracy harness and the layer benchmark on the
+GPU path (mirrors winoconv/commands.py:25-178).
 
-Algorithm names are the reference's (``f2x2``, ``f4x4``, ``f2x2-fx``,
-``f4x4-fx``), optionally suffixed with a GEMM precision, e.g. ``f4x4-fx:bf16``.
+Algorithm names are the reference's (``direct``, ``direct-fp32``, ``f2x2``,
+``f4x4``, ``f2x2-fx``, ``f4x4-fx``); the Winograd names take an optional GEMM
+precision suffix, e.g. ``f4x4-fx:bf16``.  ``fft`` (the reference's FFT
+comparison algorithm) is not on the GPU path: ValueError.
 """
 from __future__ import annotations
 
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence, Tuple
 
+from .direct import direct_forward
 from .engine import FilterCache, get_plan, winograd_forward
 from .layer import LayerConfig, builtin, gflops_direct
 from .suites import get_suite
-from .tensors import Tensor4, fill_uniform
+from .tensors import Precision, Tensor4, fill_uniform, max_abs_error, quantize_fp16
 
 BENCH_ALGOS = ("f2x2", "f4x4", "f2x2-fx", "f4x4-fx")
+DIRECT_ALGOS = ("direct", "direct-fp32")
+ACCURACY_ALGOS = ("direct-fp32", "f2x2", "f4x4")  # the reference's, minus fft
 PRECISIONS = ("fp32", "tf32", "bf16", "fp16", "fp64")
 
 
@@ -32,6 +37,11 @@ def parse_algo(algo: str) -> Tuple[int, bool, Optional[str]]:
 def run_layer(algo: str, d: Tensor4, g: Tensor4, cfg: LayerConfig,
               cache: Optional[FilterCache] = None, counter=None) -> Tensor4:
     """Dispatch one forward layer by algorithm name (commands.py:31-51)."""
+    if algo == "direct":
+        accum = Precision.FP64 if d.precision is Precision.FP64 else Precision.FP32
+        return direct_forward(d, g, cfg, accum=accum, counter=counter)
+    if algo == "direct-fp32":
+        return direct_forward(d, g, cfg, accum=Precision.FP32, counter=counter)
     m, fx, prec = parse_algo(algo)
     return winograd_forward(d, g, cfg, builtin(m, 3), cache_filters=fx, cache=cache,
                             counter=counter, prec=prec)
@@ -125,4 +135,29 @@ def cmd_bench(suite: str = "vgg-e", algo: str = "f2x2", batch: int = 1, repeats:
         total_gf += gflops_direct(cfg)
     if total_sec > 0:
         rep.add("TOTAL", algo, batch, total_sec * 1e3, total_gf / total_sec)
+    return rep
+
+
+def cmd_accuracy(suite: str = "vgg-e-accuracy", algos: Sequence[str] = ACCURACY_ALGOS,
+                 precision: str = "fp32", seed: int = 0, scale: float = 1.0) -> Report:
+    """Max abs error of each algorithm against the fp64 direct oracle, computed
+    on the GPU (commands.py:64-92).  ``precision="fp16"`` snaps both operands to
+    the binary16 grid first and keeps the oracle on the unquantized values."""
+    if precision not in ("fp32", "fp16"):
+        raise ValueError(f"precision must be fp32 or fp16, got {precision!r}")
+    for a in algos:
+        base = a.partition(":")[0]
+        if a not in ACCURACY_ALGOS and a not in DIRECT_ALGOS and base not in BENCH_ALGOS:
+            raise ValueError(f"unknown algorithm {a!r}; known: {', '.join(ACCURACY_ALGOS)}")
+    layers = get_suite(suite).scaled(scale)
+    tag = "fp32" if precision == "fp32" else Precision.FP16_SIM.value
+    rep = Report(columns=("layer", "algo", "precision", "max_abs_err"), seed=seed)
+    for i, entry in enumerate(layers.entries):
+        d, g = layer_inputs(entry.cfg, seed, i)
+        oracle = direct_forward(d.astype(Precision.FP64), g.astype(Precision.FP64), entry.cfg)
+        if precision == "fp16":
+            d, g = quantize_fp16(d), quantize_fp16(g)
+        for algo in algos:
+            y = run_layer(algo, d, g, entry.cfg)
+            rep.add(entry.label, algo, tag, max_abs_error(y, oracle))
     return rep

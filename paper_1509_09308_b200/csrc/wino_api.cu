@@ -922,6 +922,32 @@ int wino_wgrad_workspace(const wino_layer_t* layer, int prec, size_t workspace_l
   return WINO_OK;
 }
 
+int wino_direct_forward(const wino_layer_t* layer, int in_prec, int acc_prec, const void* d,
+                        const void* g, void* y, void* stream) {
+  g_err.clear();
+  if (!layer || !d || !g || !y) {
+    set_error("null argument");
+    return WINO_EINVAL;
+  }
+  const wino_layer_t& L = *layer;
+  if (L.N < 1 || L.C < 1 || L.H < 1 || L.W < 1 || L.K < 1 || L.R < 1 || L.S < 1 || L.pad < 0) {
+    set_error("N, C, H, W, K, R, S must be >= 1 and pad >= 0");
+    return WINO_EINVAL;
+  }
+  if ((in_prec != kFP32 && in_prec != kFP64) || (acc_prec != kFP32 && acc_prec != kFP64)) {
+    set_error("accumulator precision must be fp32 or fp64");  // direct.py:76-79
+    return WINO_EINVAL;
+  }
+  const int oh = L.H + 2 * L.pad - L.R + 1, ow = L.W + 2 * L.pad - L.S + 1;
+  if (oh < 1 || ow < 1) {
+    set_error("output dimensions must be >= 1");
+    return WINO_EINVAL;
+  }
+  cudaError_t e = launch_direct(in_prec, acc_prec, d, g, y, L.N, L.C, L.H, L.W, L.K, L.R, L.S,
+                                L.pad, oh, ow, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? WINO_OK : cuda_fail(e, "direct convolution");
+}
+
 int wino_grad_weights(const wino_layer_t* layer, int prec, const void* d, const void* dy,
                       void* dg, void* workspace, size_t workspace_bytes, size_t workspace_limit,
                       void* stream) {

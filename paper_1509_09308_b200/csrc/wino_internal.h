@@ -89,6 +89,12 @@ int gemm_device_sms();
 bool gemm_tmem_a_enabled();  // 3xTF32 A operand through TMEM (WINO_NO_TMEM_A=1 disables)
 // Tensor-core (tcgen05) GEMM for FP32/TF32/BF16/FP16, CUDA-core fp64 for FP64.
 cudaError_t launch_batched_gemm(int prec, const GemmArgs& a, cudaStream_t s);
+
+// Direct correlation (reference order and rounding), input fp32/fp64 ->
+// accumulator/output fp32/fp64 (wino_direct.cu).
+cudaError_t launch_direct(int in_prec, int acc_prec, const void* d, const void* g, void* y, int N,
+                          int C, int H, int W, int K, int R, int S, int pad, int oh, int ow,
+                          cudaStream_t s);
 int gemm_kernels_per_launch(int prec);
 
 // Fused Winograd-GEMM (wino_fused.cu): input transform in the producer warps,

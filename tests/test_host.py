@@ -233,3 +233,9 @@ def test_planner_decisions_vgg():
     assert conv12["num_chunks"] > 1 and conv12["m_bytes_per_elem"] == 4
     # large-P 3xTF32: workspace holds U as hi/lo planes (2 x u_bytes) + two V/M chunk sets
     assert conv12["workspace_bytes"] >= 2 * conv12["u_bytes"]
+
+
+def test_cli_accuracy_usage_errors():
+    from paper_1509_09308_b200.__main__ import main
+    assert main(["accuracy", "--algos", "fft"]) == 1
+    assert main(["accuracy", "--algos", "f2x2", "--suite", "no-such-suite"]) == 1
