@@ -589,7 +589,14 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
   const bool may_overlap = !timer && !p->smallc && p->path != kPathFused &&
                            getenv("WINO_NO_OVERLAP") == nullptr;
   const bool chunk_overlap = may_overlap && p->overlap && p->path == kPathStaged;
-  if (may_overlap && (!U || chunk_overlap)) {
+  // Non-FX single-chunk staged plans with 16-bit operands: filter and input
+  // transforms in one launch (no side stream, one predecessor for the GEMM).
+  // Measured: F4 bf16 N=1 VGG-E 0.328 -> 0.314 ms; for the fp32 (3xTF32) plans
+  // the side-stream arrangement stays faster (0.385 vs 0.389 ms), so they keep it.
+  const bool combined = !U && !timer && p->path == kPathStaged && !p->smallc &&
+                        (p->prec == kBF16 || p->prec == kFP16) && p->num_chunks == 1 &&
+                        transforms_combinable(p->prec, p->L.W, p->L.pad);
+  if (may_overlap && !combined && (!U || chunk_overlap)) {
     side = side_stream(s);
     if (side && (cudaEventRecord(side->fork, s) != cudaSuccess ||
                  cudaStreamWaitEvent(side->st, side->fork, 0) != cudaSuccess))
@@ -602,7 +609,16 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
   // the two instead of behind an event join.
   bool in_side = false;
   const bool u_split = !U && p->u_split2;  // U computed here as hi / lo planes
-  if (!U) {
+  if (combined) {
+    const wino_layer_t& Lc = p->L;
+    cudaError_t e = launch_transforms(p->m, p->prec, d, ws + p->u_ws, Lc.N, Lc.C, Lc.H, Lc.W,
+                                      Lc.pad, p->th, p->tw, p->rows_total, p->P, p->c_pad, g, ws,
+                                      Lc.K, u_split, s);
+    if (e != cudaSuccess) return cuda_fail(e, "filter + input transforms");
+    in_side = true;  // chunk 0's V is already being formed
+    U = ws;
+    ws += p->u_ws;
+  } else if (!U) {
     in_side = side && p->path == kPathStaged && p->num_chunks == 1 && !chunk_overlap &&
               static_cast<long long>(p->L.K) > p->P;
     if (in_side) {

@@ -41,6 +41,13 @@ inline int op_splits(int) { return 1; }
 cudaError_t launch_filter_transform(int m, int prec, const void* g, void* U, int K, int C,
                                     int c_pad, cudaStream_t s, bool split2 = false);
 
+// Filter transform + single-chunk TMA input transform in one launch (non-FX,
+// W % 4 == 0, pad <= 3, not fp64): V for tile rows [0, rows), U as above.
+bool transforms_combinable(int prec, int W, int pad);
+cudaError_t launch_transforms(int m, int prec, const void* d, void* V, int N, int C, int H, int W,
+                              int pad, int th, int tw, int rows, long long Pc, int c_pad,
+                              const void* g, void* U, int K, bool split2, cudaStream_t s);
+
 // d (N,C,H,W) -> V [nsplit][alpha^2][Pc][c_pad] for tile rows [row0, row0+rows)
 cudaError_t launch_input_transform(int m, int prec, const void* d, void* V, int N, int C, int H,
                                    int W, int pad, int th, int tw, int row0, int rows,

@@ -66,19 +66,17 @@ __device__ __forceinline__ void store_tile(TA* dst, int ow, int vr, int vc, cons
 // give strided warp loads), then thread t forms G g G^T for pairs t, t+256, ... and writes
 // U[s][comp][k][c] with c fastest (coalesced across the warp).
 // (engine.py:104-114)
-template <int M, int PREC, int FPT, bool SPLIT2 = false>
-__global__ void __launch_bounds__(256) filter_transform_kernel(
-    const typename OpStore<PREC>::T* __restrict__ g, void* __restrict__ U, int K, int C,
-    int c_pad) {
+// One block's work (block index `blk`, staging buffer `sg` of 256*FPT*9 T).
+template <int M, int PREC, int FPT, bool SPLIT2>
+__device__ __forceinline__ void filter_block(const typename OpStore<PREC>::T* __restrict__ g,
+                                             void* __restrict__ U, int K, int C, int c_pad,
+                                             int blk, typename OpStore<PREC>::T* sg) {
   using T = typename OpStore<PREC>::T;
   using A = Alg<M>;
   constexpr int AL = A::alpha;
   constexpr int NP = 256 * FPT;  // pairs per block
-  __shared__ __align__(16) T sg[NP * 9];
-  griddep_launch();
-  griddep_wait();
   const long long total = static_cast<long long>(K) * C;
-  const long long t0 = static_cast<long long>(blockIdx.x) * NP;
+  const long long t0 = static_cast<long long>(blk) * NP;
   const int nloc = static_cast<int>(min(static_cast<long long>(NP), total - t0));
   const T* src = g + t0 * 9;
   constexpr int VE = 16 / sizeof(T);  // elements per 16-byte load
@@ -132,6 +130,17 @@ __global__ void __launch_bounds__(256) filter_transform_kernel(
         idx += cstride;
       }
   }
+}
+
+template <int M, int PREC, int FPT, bool SPLIT2 = false>
+__global__ void __launch_bounds__(256) filter_transform_kernel(
+    const typename OpStore<PREC>::T* __restrict__ g, void* __restrict__ U, int K, int C,
+    int c_pad) {
+  using T = typename OpStore<PREC>::T;
+  __shared__ __align__(16) T sg[256 * FPT * 9];
+  griddep_launch();
+  griddep_wait();
+  filter_block<M, PREC, FPT, SPLIT2>(g, U, K, C, c_pad, blockIdx.x, sg);
 }
 
 // ============================================================= input transform
@@ -683,25 +692,21 @@ __device__ __forceinline__ void load_patch(const float* sc, int xwb, int base, f
   }
 }
 
+// One block's work: box (bx, by, bz) of the chunk, staged at `s` with `bar`.
 template <int M, int PREC, int SH>
-__global__ void __launch_bounds__(256) input_transform_tma_kernel(
-    const __grid_constant__ CUtensorMap tmD, void* __restrict__ V, int C, int pad, int th,
-    int tw, int row0, long long Pc, int c_pad) {
+__device__ __forceinline__ void input_tma_block(const CUtensorMap* tmD, void* __restrict__ V,
+                                                int C, int pad, int th, int tw, int row0,
+                                                long long Pc, int c_pad, int bx, int by, int bz,
+                                                float* s, uint64_t& bar) {
   using A = Alg<M>;
   using Cfg = InTma<M, SH>;
   constexpr int AL = A::alpha;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  float* s = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                      ~static_cast<uintptr_t>(1023));
-  __shared__ uint64_t bar;
-
-  const int row = row0 + blockIdx.y;
+  const int row = row0 + by;
   const int n = row / th;
   const int ty = row - n * th;
-  const int tx0 = blockIdx.x * Cfg::tpx;
-  const int c0 = blockIdx.z * 32;
+  const int tx0 = bx * Cfg::tpx;
+  const int c0 = bz * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  griddep_launch();
   if (threadIdx.x == 0) {
     ptx::mbar_init(&bar, 1);
     ptx::fence_mbar_init();
@@ -710,7 +715,7 @@ __global__ void __launch_bounds__(256) input_transform_tma_kernel(
   griddep_wait();
   if (threadIdx.x == 0) {
     ptx::mbar_arrive_expect_tx(&bar, Cfg::bytes);
-    ptx::tma_load_4d(s, &tmD, &bar, M * tx0 - pad - SH, M * ty - pad, c0, n);
+    ptx::tma_load_4d(s, tmD, &bar, M * tx0 - pad - SH, M * ty - pad, c0, n);
   }
   ptx::mbar_wait(&bar, 0);
 
@@ -739,7 +744,7 @@ __global__ void __launch_bounds__(256) input_transform_tma_kernel(
       bt6_2d(in, out);
     else
       sandwich<float, AL, AL>(in, out, [](int i, int j) { return A::BT(i, j); });
-    const long long p = static_cast<long long>(blockIdx.y) * tw + tx0 + t;
+    const long long p = static_cast<long long>(by) * tw + tx0 + t;
     size_t idx = static_cast<size_t>(p) * c_pad + c;
 #pragma unroll
     for (int xi = 0; xi < AL; ++xi)
@@ -748,6 +753,48 @@ __global__ void __launch_bounds__(256) input_transform_tma_kernel(
         OpStore<PREC>::put(V, idx, plane_v, out[xi][nu]);
         idx += comp_stride;
       }
+  }
+}
+
+template <int M, int PREC, int SH>
+__global__ void __launch_bounds__(256) input_transform_tma_kernel(
+    const __grid_constant__ CUtensorMap tmD, void* __restrict__ V, int C, int pad, int th,
+    int tw, int row0, long long Pc, int c_pad) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* s = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                      ~static_cast<uintptr_t>(1023));
+  __shared__ uint64_t bar;
+  griddep_launch();
+  input_tma_block<M, PREC, SH>(&tmD, V, C, pad, th, tw, row0, Pc, c_pad, blockIdx.x, blockIdx.y,
+                               blockIdx.z, s, bar);
+}
+
+// Filter transform and (single-chunk) TMA input transform in ONE launch:
+// blocks [0, n_in) take input boxes, the rest take 1024 (k, c) filter pairs.
+// Saves the side-stream fork/join and a launch per layer; the GEMM follows
+// in-stream behind one predecessor (PDL).
+template <int M, int PREC, int SH, bool SPLIT2>
+__global__ void __launch_bounds__(256) transforms_kernel(
+    const __grid_constant__ CUtensorMap tmD, void* __restrict__ V, int C, int pad, int th,
+    int tw, int rows, long long Pc, int c_pad, int nx, int ncb,
+    const typename OpStore<PREC>::T* __restrict__ g, void* __restrict__ U, int K) {
+  using T = typename OpStore<PREC>::T;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ uint64_t bar;
+  griddep_launch();
+  const int n_in = nx * rows * ncb;
+  const int b = blockIdx.x;
+  if (b < n_in) {
+    float* s = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                        ~static_cast<uintptr_t>(1023));
+    const int bx = b % nx, r = b / nx;
+    input_tma_block<M, PREC, SH>(&tmD, V, C, pad, th, tw, 0, Pc, c_pad, bx, r % rows, r / rows,
+                                 s, bar);
+  } else {
+    griddep_wait();
+    T* sg = reinterpret_cast<T*>((reinterpret_cast<uintptr_t>(smem_raw) + 15) &
+                                 ~static_cast<uintptr_t>(15));
+    filter_block<M, PREC, 4, SPLIT2>(g, U, K, C, c_pad, b - n_in, sg);
   }
 }
 
@@ -770,6 +817,91 @@ static cudaError_t input_tma_launch(const void* d, void* V, int N, int C, int H,
   launch_k(kern, grid, dim3(256), static_cast<size_t>(Cfg::bytes + 1024), s, tmD, V, C, pad, th,
            tw, row0, Pc, c_pad);
   return cudaGetLastError();
+}
+
+template <int M, int PREC, int SH, bool SPLIT2>
+static cudaError_t transforms_launch(const void* d, void* V, int N, int C, int H, int W, int pad,
+                                     int th, int tw, int rows, long long Pc, int c_pad,
+                                     const void* g, void* U, int K, cudaStream_t s) {
+  using Cfg = InTma<M, SH>;
+  using T = typename OpStore<PREC>::T;
+  alignas(64) CUtensorMap tmD;
+  if (!encode_tmap_nchw_f32(&tmD, d, N, C, H, W, Cfg::xwb, Cfg::rows, 32))
+    return cudaErrorInvalidValue;
+  auto kern = transforms_kernel<M, PREC, SH, SPLIT2>;
+  constexpr size_t in_smem = Cfg::bytes + 1024;
+  constexpr size_t f_smem = 256 * 4 * 9 * sizeof(T) + 16;
+  constexpr size_t smem = in_smem > f_smem ? in_smem : f_smem;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    max_carveout(kern);
+    configured = true;
+  }
+  const int nx = (tw + Cfg::tpx - 1) / Cfg::tpx, ncb = (C + 31) / 32;
+  const long long nf = (static_cast<long long>(K) * C + 1023) / 1024;
+  const long long blocks = static_cast<long long>(nx) * rows * ncb + nf;
+  if (blocks > 0x7fffffffLL) return cudaErrorInvalidValue;
+  launch_k(kern, dim3(static_cast<unsigned>(blocks)), dim3(256), smem, s, tmD, V, C, pad, th, tw,
+           rows, Pc, c_pad, nx, ncb, static_cast<const T*>(g), U, K);
+  return cudaGetLastError();
+}
+
+template <int M, int PREC>
+static cudaError_t transforms_sh(const void* d, void* V, int N, int C, int H, int W, int pad,
+                                 int th, int tw, int rows, long long Pc, int c_pad, const void* g,
+                                 void* U, int K, bool split2, cudaStream_t s) {
+  const int sh = (4 - pad % 4) % 4;
+#define WINO_TR(SHV, SP) \
+  return transforms_launch<M, PREC, SHV, SP>(d, V, N, C, H, W, pad, th, tw, rows, Pc, c_pad, g, U, K, s)
+  if (split2) {
+    if constexpr (PREC == kFP32) {
+      switch (sh) {
+        case 0: WINO_TR(0, true);
+        case 1: WINO_TR(1, true);
+        case 2: WINO_TR(2, true);
+        default: WINO_TR(3, true);
+      }
+    }
+    return cudaErrorInvalidValue;
+  }
+  switch (sh) {
+    case 0: WINO_TR(0, false);
+    case 1: WINO_TR(1, false);
+    case 2: WINO_TR(2, false);
+    default: WINO_TR(3, false);
+  }
+#undef WINO_TR
+}
+
+bool transforms_combinable(int prec, int W, int pad) {
+  return prec != kFP64 && W % 4 == 0 && pad <= 3 && getenv("WINO_NO_TMA_INPUT") == nullptr &&
+         getenv("WINO_NO_COMBINED") == nullptr;
+}
+
+cudaError_t launch_transforms(int m, int prec, const void* d, void* V, int N, int C, int H, int W,
+                              int pad, int th, int tw, int rows, long long Pc, int c_pad,
+                              const void* g, void* U, int K, bool split2, cudaStream_t s) {
+  if (!transforms_combinable(prec, W, pad)) return cudaErrorInvalidValue;
+#define WINO_TP(MM, P) \
+  return transforms_sh<MM, P>(d, V, N, C, H, W, pad, th, tw, rows, Pc, c_pad, g, U, K, split2, s)
+  if (m == 2) {
+    switch (prec) {
+      case kFP32: WINO_TP(2, kFP32);
+      case kTF32: WINO_TP(2, kTF32);
+      case kBF16: WINO_TP(2, kBF16);
+      case kFP16: WINO_TP(2, kFP16);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  switch (prec) {
+    case kFP32: WINO_TP(4, kFP32);
+    case kTF32: WINO_TP(4, kTF32);
+    case kBF16: WINO_TP(4, kBF16);
+    case kFP16: WINO_TP(4, kFP16);
+    default: return cudaErrorInvalidValue;
+  }
+#undef WINO_TP
 }
 
 template <int M, int PREC>
