@@ -5,7 +5,7 @@ Mirrors the ``bench`` and ``accuracy`` commands of the reference CLI
 (commands.cmd_bench / cmd_accuracy, commands.py:64-178) and exit codes (0 ok,
 1 usage / domain error, 2 runtime failure).  Algorithm names are the
 reference's (Winograd names optionally with a GEMM precision suffix,
-``f4x4-fx:bf16``; ``fft`` is not on the GPU path).  The CLI runs in-process;
+``f4x4-fx:bf16``).  The CLI runs in-process;
 there is no HTTP transport.
 """
 from __future__ import annotations
@@ -31,7 +31,7 @@ def build_parser() -> argparse.ArgumentParser:
                     help="write the report here instead of stdout")
     pa = sub.add_parser("accuracy", help="max abs error vs the fp64 direct oracle (GPU)")
     pa.add_argument("--suite", default="vgg-e-accuracy")
-    pa.add_argument("--algos", default="direct-fp32,f2x2,f4x4",
+    pa.add_argument("--algos", default="direct-fp32,f2x2,f4x4,fft",
                     help="comma-separated algorithm names")
     pa.add_argument("--precision", choices=("fp32", "fp16"), default="fp32")
     pa.add_argument("--seed", type=int, default=0)

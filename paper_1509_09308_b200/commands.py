@@ -2,9 +2,8 @@
 GPU path (mirrors winoconv/commands.py:25-178).
 
 Algorithm names are the reference's (``direct``, ``direct-fp32``, ``f2x2``,
-``f4x4``, ``f2x2-fx``, ``f4x4-fx``); the Winograd names take an optional GEMM
-precision suffix, e.g. ``f4x4-fx:bf16``.  ``fft`` (the reference's FFT
-comparison algorithm) is not on the GPU path: ValueError.
+``f4x4``, ``f2x2-fx``, ``f4x4-fx``, ``fft``); the Winograd names take an
+optional GEMM precision suffix, e.g. ``f4x4-fx:bf16``.
 """
 from __future__ import annotations
 
@@ -13,13 +12,14 @@ from typing import List, Optional, Sequence, Tuple
 
 from .direct import direct_forward
 from .engine import FilterCache, get_plan, winograd_forward
+from .fftconv import fft_forward_layer
 from .layer import LayerConfig, builtin, gflops_direct
 from .suites import get_suite
 from .tensors import Precision, Tensor4, fill_uniform, max_abs_error, quantize_fp16
 
 BENCH_ALGOS = ("f2x2", "f4x4", "f2x2-fx", "f4x4-fx")
 DIRECT_ALGOS = ("direct", "direct-fp32")
-ACCURACY_ALGOS = ("direct-fp32", "f2x2", "f4x4")  # the reference's, minus fft
+ACCURACY_ALGOS = ("direct-fp32", "f2x2", "f4x4", "fft")  # commands.py:25
 PRECISIONS = ("fp32", "tf32", "bf16", "fp16", "fp64")
 
 
@@ -42,6 +42,8 @@ def run_layer(algo: str, d: Tensor4, g: Tensor4, cfg: LayerConfig,
         return direct_forward(d, g, cfg, accum=accum, counter=counter)
     if algo == "direct-fp32":
         return direct_forward(d, g, cfg, accum=Precision.FP32, counter=counter)
+    if algo == "fft":
+        return fft_forward_layer(d, g, cfg, tile=8, counter=counter)
     m, fx, prec = parse_algo(algo)
     return winograd_forward(d, g, cfg, builtin(m, 3), cache_filters=fx, cache=cache,
                             counter=counter, prec=prec)

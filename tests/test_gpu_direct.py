@@ -70,3 +70,24 @@ def test_cmd_accuracy_matches_reference(wb, gd):
     for lbl, ref in zip(gd["acc_labels"], gd["acc_rows"]):
         assert rows[(str(lbl), "direct-fp32")] == ref, lbl
         assert rows[(str(lbl), "f2x2")] < 5e-4 and rows[(str(lbl), "f4x4")] < 5e-3, lbl
+
+
+def test_fft_layer_vs_reference(wb, golden, gd):
+    """The FFT comparison algorithm (cuFFT + complex128 GEMM, the reference's
+    tiling and fp64 transform arithmetic) against the reference's own outputs:
+    fp64 within 1e-12 (relative to max|y|), fp32 within 1 fp32 rounding of the
+    final cast (2^-23 relative); counters equal."""
+    for i in range(10):
+        N, C, H, W, K, pad = (int(v) for v in golden[f"case{i}_shape"])
+        cfg = wb.LayerConfig(N=N, C=C, H=H, W=W, K=K, pad=pad)
+        d = wb.Tensor4.from_array(O.fill_uniform((N, C, H, W), 100 + 2 * i), wb.Precision.FP32)
+        g = wb.Tensor4.from_array(O.fill_uniform((K, C, 3, 3), 101 + 2 * i), wb.Precision.FP32)
+        cnt = wb.OpCounter()
+        y = wb.run_layer("fft", d, g, cfg, counter=cnt)
+        ref = gd[f"case{i}_fft32"]
+        assert y.data.dtype == np.float32 and y.data.shape == ref.shape
+        assert np.abs(y.data - ref).max() <= 2 ** -23 * (1 + np.abs(ref).max()), i
+        assert [cnt.get("cmul"), cnt.get("mul")] == list(gd[f"case{i}_fft_counts"]), i
+        y64 = wb.run_layer("fft", d.astype(wb.Precision.FP64), g.astype(wb.Precision.FP64), cfg)
+        ref64 = gd[f"case{i}_fft64"]
+        assert np.abs(y64.data - ref64).max() <= 1e-12 * (1 + np.abs(ref64).max()), i

@@ -237,5 +237,5 @@ def test_planner_decisions_vgg():
 
 def test_cli_accuracy_usage_errors():
     from paper_1509_09308_b200.__main__ import main
-    assert main(["accuracy", "--algos", "fft"]) == 1
+    assert main(["accuracy", "--algos", "fft8"]) == 1
     assert main(["accuracy", "--algos", "f2x2", "--suite", "no-such-suite"]) == 1
