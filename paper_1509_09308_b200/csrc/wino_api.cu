@@ -607,7 +607,7 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
   // the input transform goes to the side stream and the filter transform stays
   // in-stream, so the GEMM launches programmatically (PDL) behind the longer of
   // the two instead of behind an event join.
-  bool in_side = false;
+  bool input_enqueued = false;  // chunk 0's input transform already launched
   const bool u_split = !U && p->u_split2;  // U computed here as hi / lo planes
   if (combined) {
     const wino_layer_t& Lc = p->L;
@@ -615,13 +615,14 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
                                       Lc.pad, p->th, p->tw, p->rows_total, p->P, p->c_pad, g, ws,
                                       Lc.K, u_split, s);
     if (e != cudaSuccess) return cuda_fail(e, "filter + input transforms");
-    in_side = true;  // chunk 0's V is already being formed
+    input_enqueued = true;
     U = ws;
     ws += p->u_ws;
   } else if (!U) {
-    in_side = side && p->path == kPathStaged && p->num_chunks == 1 && !chunk_overlap &&
-              static_cast<long long>(p->L.K) > p->P;
+    const bool in_side = side && p->path == kPathStaged && p->num_chunks == 1 &&
+                         !chunk_overlap && static_cast<long long>(p->L.K) > p->P;
     if (in_side) {
+      input_enqueued = true;
       cudaError_t e = launch_input_transform(p->m, p->prec, d, ws + p->u_ws, p->L.N, p->L.C,
                                              p->L.H, p->L.W, p->L.pad, p->th, p->tw, 0,
                                              p->rows_total, p->P, p->c_pad, side->st);
@@ -717,7 +718,7 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
     unsigned char* V = ws + bi * vm;
     unsigned char* Mb = V + p->v_bytes;
     cudaError_t e = cudaSuccess;
-    if (!(in_side && ch == 0)) {  // (in_side: already enqueued on the side stream)
+    if (!(input_enqueued && ch == 0)) {
       e = launch_input_transform(p->m, p->prec, d, V, L.N, L.C, L.H, L.W, L.pad, p->th, p->tw,
                                  row0, rows, Pc, p->c_pad, cs);
       if (e != cudaSuccess) return cuda_fail(e, "input transform");

@@ -30,4 +30,11 @@ $T 300 ncu --set full --clock-control none --import-source on -k regex:wgemm -s 
    -o $OUT/gemm_conv32_f4_bf16_n64 python tools/prof_layer.py conv3.2 4 bf16 64 2 > /dev/null 2>&1
 WINO_PATH=hybrid $T 300 ncu --set full --clock-control none --import-source on -k regex:wfused -s 1 -c 1 \
    -o $OUT/fused_hybrid_conv32_f4_bf16_n64 python tools/prof_layer.py conv3.2 4 bf16 64 2 > /dev/null 2>&1
+# summaries on the box; keep only the two source-level reports (gpurun copies back <= 64 MiB)
+for r in $OUT/*.ncu-rep; do
+  b=$(basename $r .ncu-rep)
+  python tools/ncu_summary.py $r > $OUT/ncu_$b.txt 2>&1
+  python tools/ncu_raw_summary.py $r >> $OUT/ncu_$b.txt 2>&1
+  case $b in gemm_conv42_f2_fp32_n1|input_conv12_f4_bf16_n64) ;; *) rm -f $r ;; esac
+done
 ls -la $OUT
