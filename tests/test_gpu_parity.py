@@ -364,3 +364,20 @@ def test_cta_pair_gemm_variant_parity():
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [l for l in out.stdout.splitlines() if l.startswith("N=")]
     assert len(lines) == 5 and all(l.endswith("OK") for l in lines), out.stdout
+
+
+@pytest.mark.parametrize("pad", [0, 2, 3, 5])
+def test_padding_variants(wb, pad):
+    """Zero padding other than 1 (the TMA input box shifts by (-pad) mod 4, pad
+    > 3 takes the generic staging kernel), F2 and F4, fp32 and bf16, W % 4 == 0
+    and not."""
+    for (H, W) in ((16, 20), (13, 10)):
+        d = O.fill_uniform((2, 24, H, W), 90 + pad)
+        g = O.fill_uniform((12, 24, 3, 3), 91 + pad)
+        ref = O.direct_forward(d, g, pad)
+        for m in (2, 4):
+            y = _run(wb, d, g, pad, m)
+            assert y.shape == ref.shape
+            assert O.max_abs_error(y, ref) < (5e-4 if m == 2 else 5e-3), (pad, H, W, m)
+            yb = _run(wb, d, g, pad, m, prec="bf16")
+            assert O.max_abs_error(yb, ref) / np.abs(ref).max() <= REL_TOL[("bf16", m)]
