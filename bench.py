@@ -291,7 +291,8 @@ def run_gpu(args) -> None:
                            y=y, ws=ws, U=U, d_host=d_host, y_host=y_host,
                            gf=gflop_direct(B, C, H, K)))
     gf_step = sum(L["gf"] * L["depth"] for L in layers)
-    launches_step = sum(L["depth"] * (L["plan"].info["launches_per_forward"] + (0 if fx else 1))
+    launches_step = sum(L["depth"] * (L["plan"].info["launches_per_forward"] +
+                                      (0 if fx or L["plan"].info["combined_transforms"] else 1))
                         for L in layers)
 
     stream = torch.cuda.Stream(device=dev)

@@ -74,6 +74,7 @@ typedef struct {
   int fused;                  /* 1: fused Winograd-GEMM kernel (no V/M staging)  */
   int fused_splits;           /* split-C factor of the fused kernel              */
   int m_bytes_per_elem;       /* staged M element: 4 (fp32), 2 (bf16 GEMM), 8   */
+  int combined_transforms;    /* non-FX forwards launch filter+input together   */
 } wino_plan_info_t;
 
 /* Create a plan.  m in {2,4} (F(2x2,3x3), F(4x4,3x3)); R == S == 3.

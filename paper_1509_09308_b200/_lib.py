@@ -49,7 +49,7 @@ class PlanInfo(ctypes.Structure):
         ("launches_per_forward", ctypes.c_int), ("fused_small_c", ctypes.c_int),
         ("multiplies", ctypes.c_longlong),
         ("fused", ctypes.c_int), ("fused_splits", ctypes.c_int),
-        ("m_bytes_per_elem", ctypes.c_int),
+        ("m_bytes_per_elem", ctypes.c_int), ("combined_transforms", ctypes.c_int),
     ]
 
     def as_dict(self) -> dict:

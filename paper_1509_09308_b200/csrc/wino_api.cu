@@ -438,6 +438,13 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
   return WINO_OK;
 }
 
+// Non-FX forwards of this plan launch the filter and input transforms as one
+// kernel (staged, single chunk, 16-bit operands, TMA-eligible input).
+static bool plan_combines_transforms(const wino_plan_s* p) {
+  return p->path == kPathStaged && !p->smallc && (p->prec == kBF16 || p->prec == kFP16) &&
+         p->num_chunks == 1 && transforms_combinable(p->prec, p->L.W, p->L.pad);
+}
+
 int wino_plan_destroy(wino_plan_t plan) {
   delete plan;
   return WINO_OK;
@@ -477,6 +484,7 @@ int wino_plan_get_info(wino_plan_t p, wino_plan_info_t* info) {
   info->fused = p->path;
   info->fused_splits = p->fsplits;
   info->m_bytes_per_elem = p->m_es;
+  info->combined_transforms = plan_combines_transforms(p) ? 1 : 0;
   info->fused_small_c = p->smallc ? 1 : 0;
   info->multiplies = p->P * p->L.C * static_cast<long long>(p->L.K) * p->a2;
   return WINO_OK;
@@ -593,9 +601,7 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
   // transforms in one launch (no side stream, one predecessor for the GEMM).
   // Measured: F4 bf16 N=1 VGG-E 0.328 -> 0.314 ms; for the fp32 (3xTF32) plans
   // the side-stream arrangement stays faster (0.385 vs 0.389 ms), so they keep it.
-  const bool combined = !U && !timer && p->path == kPathStaged && !p->smallc &&
-                        (p->prec == kBF16 || p->prec == kFP16) && p->num_chunks == 1 &&
-                        transforms_combinable(p->prec, p->L.W, p->L.pad);
+  const bool combined = !U && !timer && plan_combines_transforms(p);
   if (may_overlap && !combined && (!U || chunk_overlap)) {
     side = side_stream(s);
     if (side && (cudaEventRecord(side->fork, s) != cudaSuccess ||
