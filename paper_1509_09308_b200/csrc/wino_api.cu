@@ -287,7 +287,7 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
   const size_t budget = workspace_limit ? workspace_limit : kDefaultWorkspace;
   // bf16 GEMM: M is staged in bf16.  The accumulation stays fp32 (TMEM); the one
   // extra rounding of M is of the size of the bf16 operand roundings of U and V
-  // that already dominate the variant's error (~7% rms added),
+  // that already dominate the variant's error (measured +22% rms),
   // and it halves the largest staged tensor.  WINO_M_FP32=1 keeps fp32 M.
   p->m_es = (prec == kBF16 && getenv("WINO_M_FP32") == nullptr) ? 2 : p->acc_bytes;
   const size_t per_tile = static_cast<size_t>(p->nsplit) * p->a2 * p->c_pad * p->esize +
