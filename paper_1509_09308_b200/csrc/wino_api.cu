@@ -860,10 +860,22 @@ struct WgPlan {
   int oh, ow, gh, gw;
   long long B, nb, b_pad;
   int nchunks, esize, nsplit, acc_bytes, bn, splits;
+  int total_slices;  // M slices over all chunks (keep_all) -- each chunk's effective splits
+  int keep_all;      // every chunk keeps its own slices; else a running sum is folded per chunk
   long long m_ld;
-  size_t u_bytes, v_bytes, m_bytes;
+  size_t u_bytes, v_bytes, m_bytes, slice_bytes;
 };
-constexpr size_t kWgradDefaultWorkspace = 256ull << 20;
+// 1 GB: VGG-E layers at N = 8 run as one tile chunk (no per-chunk wave tails).
+constexpr size_t kWgradDefaultWorkspace = 1ull << 30;
+
+// Split count the GEMM actually runs for a chunk of nb tiles: the last split
+// never ends up empty (the kernel's epilogue needs at least one k-block).
+int wgrad_effective_splits(int prec, long long nb, int splits) {
+  const int nkb = gemm_num_kblocks(prec, static_cast<int>(nb));
+  if (splits <= 1 || nkb <= 1) return 1;
+  const int kbps = (nkb + splits - 1) / splits;
+  return (nkb + kbps - 1) / kbps;
+}
 
 int wgrad_plan(const wino_layer_t* layer, int prec, size_t limit, WgPlan* w) {
   if (!layer) {
@@ -907,25 +919,48 @@ int wgrad_plan(const wino_layer_t* layer, int prec, size_t limit, WgPlan* w) {
   int bn = prec == kFP32 ? 128 : 256;
   while (bn > 32 && bn / 2 >= L.K) bn /= 2;
   w->bn = bn;
+  w->m_ld = static_cast<long long>(align_up(static_cast<size_t>(L.C), 4));
+  w->slice_bytes = static_cast<size_t>(16) * L.K * w->m_ld * w->acc_bytes;
+  // Split the tile reduction so the GEMM's work units fill whole waves: cost =
+  // waves x (k-steps per unit + 2 for fill and epilogue) + each slice's HBM
+  // write and re-read (~3 MB per k-step); ties -> fewer splits.
   w->splits = 1;
   if (prec != kFP64) {
+    const int sms = gemm_device_sms();
     const int num_kb = gemm_num_kblocks(prec, static_cast<int>(nb));
     const long long units = ((L.C + 127) / 128) * ((L.K + bn - 1) / bn) * 16LL;
-    const long long target = 2LL * gemm_device_sms();
-    if (units < target && num_kb >= 4) {
-      long long sp = (target + units - 1) / units;
-      if (sp > num_kb / 2) sp = num_kb / 2;
-      const int kbps = static_cast<int>((num_kb + sp - 1) / sp);
-      w->splits = (num_kb + kbps - 1) / kbps;
+    const double slice_cost = 2.0 * static_cast<double>(w->slice_bytes) / 3e6;
+    double best = 1e30;
+    for (int sp = 1; sp <= num_kb && sp <= 512; ++sp) {
+      const int kbps = (num_kb + sp - 1) / sp;
+      const int sp_eff = (num_kb + kbps - 1) / kbps;
+      if (sp_eff != sp) continue;
+      const long long waves = (units * sp + sms - 1) / sms;
+      const double cost = static_cast<double>(waves) * (kbps + 2) + sp * slice_cost;
+      if (cost < best - 1e-9) {
+        best = cost;
+        w->splits = sp;
+      }
+    }
+    if (const char* e = getenv("WINO_WGRAD_SPLITS")) {  // tuning override
+      const int v = atoi(e);
+      if (v >= 1 && v <= num_kb) w->splits = wgrad_effective_splits(prec, nb, v);
     }
   }
-  w->m_ld = static_cast<long long>(align_up(static_cast<size_t>(L.C), 4));
+  w->total_slices = 0;
+  for (int ch = 0; ch < w->nchunks; ++ch) {
+    const long long b0 = static_cast<long long>(ch) * nb;
+    w->total_slices += wgrad_effective_splits(prec, b0 + nb <= w->B ? nb : w->B - b0, w->splits);
+  }
+  w->keep_all = (w->nchunks == 1 ||
+                 static_cast<size_t>(w->total_slices) * w->slice_bytes <= budget / 4) ? 1 : 0;
   w->u_bytes = align_up(static_cast<size_t>(w->nsplit) * 16 * L.K * w->b_pad * w->esize, 1024);
   w->v_bytes = align_up(static_cast<size_t>(w->nsplit) * 16 * L.C * w->b_pad * w->esize, 1024);
-  // one chunk's split slices, plus a running accumulator when there are
-  // several chunks (folded after every chunk: bounded memory, fixed order)
-  w->m_bytes = align_up(static_cast<size_t>(w->splits + (w->nchunks > 1 ? 1 : 0)) * 16 * L.K *
-                            w->m_ld * w->acc_bytes,
+  // keep_all: every chunk's split slices, summed once by the inverse transform;
+  // else one chunk's slices plus a running sum folded after every chunk
+  // (bounded memory).  Either way the slices are summed in one fixed order.
+  w->m_bytes = align_up((w->keep_all ? static_cast<size_t>(w->total_slices)
+                                     : static_cast<size_t>(w->splits + 1)) * w->slice_bytes,
                         1024);
   return WINO_OK;
 }
@@ -993,32 +1028,35 @@ int wino_grad_weights(const wino_layer_t* layer, int prec, const void* d, const 
   void* Uw = ws;
   void* Vw = ws + w.u_bytes;
   unsigned char* Mb = ws + w.u_bytes + w.v_bytes;
-  const size_t slice = static_cast<size_t>(16) * L.K * w.m_ld * w.acc_bytes;
-  unsigned char* acc = Mb;                                   // running sum (several chunks)
-  unsigned char* parts = w.nchunks > 1 ? Mb + slice : Mb;    // this chunk's split slices
+  const size_t slice = w.slice_bytes;
+  unsigned char* acc = Mb;  // running sum (fold mode)
+  int slot = 0;             // keep_all: next free slice
   for (int ch = 0; ch < w.nchunks; ++ch) {
     const long long b0 = static_cast<long long>(ch) * w.nb;
     const long long nb = (b0 + w.nb <= w.B) ? w.nb : w.B - b0;
+    const int sp = wgrad_effective_splits(prec, nb, w.splits);
+    unsigned char* parts = w.keep_all ? Mb + static_cast<size_t>(slot) * slice : Mb + slice;
     cudaError_t e = launch_wgrad_transforms(prec, d, dy, Uw, Vw, L.K, L.C, L.H, L.W, L.pad, w.oh,
                                             w.ow, w.gh, w.gw, b0, nb, w.b_pad, s);
     if (e != cudaSuccess) return cuda_fail(e, "weight-gradient transforms");
     // M[comp][k][c] = sum_b Uw[comp][k][b] Vw[comp][c][b]: the forward GEMM with
-    // (rows = C, reduction = tiles), partial sums in `splits` slices
+    // (rows = C, reduction = tiles), partial sums in `sp` slices
     GemmArgs ga{Vw, Uw, parts, 16, L.K, static_cast<int>(nb), static_cast<int>(w.b_pad), L.C,
-                w.bn, w.splits, w.m_ld};
+                w.bn, sp, w.m_ld};
     e = launch_batched_gemm(prec, ga, s);
     if (e != cudaSuccess) {
       if (g_err.empty()) return cuda_fail(e, "weight-gradient gemm");
       return WINO_ECUDA;
     }
-    if (w.nchunks > 1) {
-      e = launch_wgrad_accumulate(prec, acc, parts, static_cast<long long>(16) * L.K * w.m_ld,
-                                  w.splits, ch == 0 ? 1 : 0, s);
+    slot += sp;
+    if (!w.keep_all) {
+      e = launch_wgrad_accumulate(prec, acc, parts, static_cast<long long>(16) * L.K * w.m_ld, sp,
+                                  ch == 0 ? 1 : 0, s);
       if (e != cudaSuccess) return cuda_fail(e, "weight-gradient accumulate");
     }
   }
   cudaError_t e = launch_wgrad_inverse(prec, Mb, dg, L.K, L.C, w.m_ld,
-                                       w.nchunks > 1 ? 1 : w.splits, s);
+                                       w.keep_all ? w.total_slices : 1, s);
   if (e != cudaSuccess) return cuda_fail(e, "weight-gradient inverse transform");
   return WINO_OK;
 }

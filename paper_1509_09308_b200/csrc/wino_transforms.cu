@@ -1420,6 +1420,7 @@ __global__ void __launch_bounds__(256) wgrad_d_transform_kernel(
 }
 
 // dg[k][c] = A^T (sum_s M[s][.][k][c]) A, slices summed in ascending order.
+// Thread = (k, c) with all 16 components: used when K*C fills the GPU.
 template <typename TA>
 __global__ void __launch_bounds__(256) wgrad_inverse_kernel(const TA* __restrict__ Mbuf,
                                                             TA* __restrict__ dg, int K, int C,
@@ -1444,6 +1445,46 @@ __global__ void __launch_bounds__(256) wgrad_inverse_kernel(const TA* __restrict
       for (int nu = 0; nu < 4; ++nu)
         acc[xi][nu] += Ms[(xi * 4 + nu) * comp_stride + static_cast<size_t>(k) * m_ld + c];
   }
+  TA out[3][3];
+  sandwich<TA, 3, 4>(acc, out, [](int i, int j) { return Alg32::AT(i, j); });
+  TA* dst = dg + (static_cast<size_t>(k) * C + c) * 9;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) dst[i * 3 + j] = out[i][j];
+}
+
+// Same result, for small K*C with many slices (conv1.1: C = 3, tens of
+// slices): block = (16 channels c, one k), thread = (component, c), c fastest.
+// Each thread sums one M element over the slices (independent loads), then 16
+// threads apply the 4x4 -> 3x3 inverse.
+template <typename TA>
+__global__ void __launch_bounds__(256) wgrad_inverse_wide_kernel(const TA* __restrict__ Mbuf,
+                                                                 TA* __restrict__ dg, int K,
+                                                                 int C, long long m_ld,
+                                                                 int slices) {
+  griddep_launch();
+  griddep_wait();
+  __shared__ TA sm[16][17];
+  const int cl = threadIdx.x & 15, comp = threadIdx.x >> 4;
+  const int c = blockIdx.x * 16 + cl;
+  const int k = blockIdx.y;
+  const size_t comp_stride = static_cast<size_t>(K) * m_ld;
+  const size_t slice_stride = 16 * comp_stride;
+  if (c < C) {
+    const TA* p = Mbuf + comp * comp_stride + static_cast<size_t>(k) * m_ld + c;
+    TA v = p[0];
+#pragma unroll 8
+    for (int s = 1; s < slices; ++s) v += p[s * slice_stride];
+    sm[comp][cl] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x >= 16 || c >= C) return;
+  TA acc[4][4];
+#pragma unroll
+  for (int xi = 0; xi < 4; ++xi)
+#pragma unroll
+    for (int nu = 0; nu < 4; ++nu) acc[xi][nu] = sm[xi * 4 + nu][cl];
   TA out[3][3];
   sandwich<TA, 3, 4>(acc, out, [](int i, int j) { return Alg32::AT(i, j); });
   TA* dst = dg + (static_cast<size_t>(k) * C + c) * 9;
@@ -1512,13 +1553,25 @@ cudaError_t launch_wgrad_transforms(int prec, const void* d, const void* dy, voi
 
 cudaError_t launch_wgrad_inverse(int prec, const void* Mbuf, void* dg, int K, int C,
                                  long long m_ld, int slices, cudaStream_t s) {
-  const dim3 grid((C + 255) / 256, K);
-  if (prec == kFP64)
-    launch_k(wgrad_inverse_kernel<double>, grid, dim3(256), 0, s,
-             static_cast<const double*>(Mbuf), static_cast<double*>(dg), K, C, m_ld, slices);
-  else
-    launch_k(wgrad_inverse_kernel<float>, grid, dim3(256), 0, s, static_cast<const float*>(Mbuf),
-             static_cast<float*>(dg), K, C, m_ld, slices);
+  // thread per (k, c) once K*C covers the SMs a few times over; else spread
+  // the slice sums over 16x more threads
+  const bool wide = static_cast<long long>(K) * C < 64LL * 1024;
+  const dim3 grid(wide ? (C + 15) / 16 : (C + 255) / 256, K);
+  if (prec == kFP64) {
+    if (wide)
+      launch_k(wgrad_inverse_wide_kernel<double>, grid, dim3(256), 0, s,
+               static_cast<const double*>(Mbuf), static_cast<double*>(dg), K, C, m_ld, slices);
+    else
+      launch_k(wgrad_inverse_kernel<double>, grid, dim3(256), 0, s,
+               static_cast<const double*>(Mbuf), static_cast<double*>(dg), K, C, m_ld, slices);
+  } else {
+    if (wide)
+      launch_k(wgrad_inverse_wide_kernel<float>, grid, dim3(256), 0, s,
+               static_cast<const float*>(Mbuf), static_cast<float*>(dg), K, C, m_ld, slices);
+    else
+      launch_k(wgrad_inverse_kernel<float>, grid, dim3(256), 0, s,
+               static_cast<const float*>(Mbuf), static_cast<float*>(dg), K, C, m_ld, slices);
+  }
   return cudaGetLastError();
 }
 

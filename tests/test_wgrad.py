@@ -156,3 +156,22 @@ def test_chunked_and_split_tiles():
     for out in (a, b):
         assert O.max_abs_error(out, ref) < 1e-3
     assert np.abs(a - b).max() <= 1e-5 * (1 + np.abs(ref).max())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec,tol", [("fp32", 1e-5), ("bf16", 3e-2)])
+def test_small_c_many_splits(prec, tol):
+    """conv1.1-like shape (C = 3): the tile reduction is split into many
+    slices (whole waves of GEMM units); the inverse transform sums them."""
+    import torch
+    import paper_1509_09308_b200 as wb
+    cfg = wb.LayerConfig(N=2, C=3, H=64, W=64, K=64, pad=1)
+    dn = O.fill_uniform((2, 3, 64, 64), 41)
+    yn = O.fill_uniform((2, 64, 64, 64), 42)
+    ref = O.direct_grad_weights(dn, yn, 1)
+    d, dy = torch.from_numpy(dn).cuda(), torch.from_numpy(yn).cuda()
+    out = wb.grad_weights_device(d, dy, cfg, prec).cpu().numpy()
+    assert O.max_abs_error(out, ref) / np.abs(ref).max() <= tol
+    # the fold path (running sum per chunk) agrees with the keep-all path
+    b = wb.grad_weights_device(d, dy, cfg, prec, workspace_limit=1 << 20).cpu().numpy()
+    assert np.abs(out - b).max() <= 1e-5 * (1 + np.abs(ref).max())
