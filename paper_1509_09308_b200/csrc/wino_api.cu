@@ -862,6 +862,8 @@ struct WgPlan {
   int nchunks, esize, nsplit, acc_bytes, bn, splits;
   int total_slices;  // M slices over all chunks (keep_all) -- each chunk's effective splits
   int keep_all;      // every chunk keeps its own slices; else a running sum is folded per chunk
+  int smallc;        // C <= 4: one CUDA-core pass (wgrad_smallc_kernel), no staging
+  int nblk;          // smallc: blocks = M slices
   long long m_ld;
   size_t u_bytes, v_bytes, m_bytes, slice_bytes;
 };
@@ -947,6 +949,23 @@ int wgrad_plan(const wino_layer_t* layer, int prec, size_t limit, WgPlan* w) {
       if (v >= 1 && v <= num_kb) w->splits = wgrad_effective_splits(prec, nb, v);
     }
   }
+  // C <= 4: the tensor-core GEMM would waste 125 of 128 rows and stage 16 x K
+  // values per tile through HBM; the small-C kernel reads d and dY once
+  w->smallc = (L.C <= 4 && prec != kFP64 && !getenv("WINO_NO_WGRAD_SMALLC")) ? 1 : 0;
+  if (w->smallc) {
+    const long long groups = (w->B + 31) / 32;
+    const int per_y = (2 * gemm_device_sms()) / ((L.K + 63) / 64);
+    w->nblk = static_cast<int>(groups < per_y ? groups : (per_y > 0 ? per_y : 1));
+    w->nb = w->B;
+    w->nchunks = 1;
+    w->splits = 1;
+    w->total_slices = w->nblk;
+    w->keep_all = 1;
+    w->u_bytes = w->v_bytes = 0;
+    w->m_bytes = align_up(static_cast<size_t>(w->nblk + 1) * w->slice_bytes, 1024);
+    return WINO_OK;
+  }
+  w->nblk = 0;
   w->total_slices = 0;
   for (int ch = 0; ch < w->nchunks; ++ch) {
     const long long b0 = static_cast<long long>(ch) * nb;
@@ -1029,6 +1048,15 @@ int wino_grad_weights(const wino_layer_t* layer, int prec, const void* d, const 
   void* Vw = ws + w.u_bytes;
   unsigned char* Mb = ws + w.u_bytes + w.v_bytes;
   const size_t slice = w.slice_bytes;
+  if (w.smallc) {
+    unsigned char* summed = Mb + static_cast<size_t>(w.nblk) * slice;
+    cudaError_t e = launch_wgrad_smallc(prec, d, dy, Mb, summed, L.K, L.C, L.H, L.W, L.pad, w.oh,
+                                        w.ow, w.gh, w.gw, w.B, w.m_ld, w.nblk, s);
+    if (e != cudaSuccess) return cuda_fail(e, "small-C weight gradient");
+    e = launch_wgrad_inverse(prec, summed, dg, L.K, L.C, w.m_ld, 1, s);
+    if (e != cudaSuccess) return cuda_fail(e, "weight-gradient inverse transform");
+    return WINO_OK;
+  }
   unsigned char* acc = Mb;  // running sum (fold mode)
   int slot = 0;             // keep_all: next free slice
   for (int ch = 0; ch < w.nchunks; ++ch) {

@@ -76,6 +76,13 @@ cudaError_t launch_wgrad_transforms(int prec, const void* d, const void* dy, voi
                                     cudaStream_t s);
 cudaError_t launch_wgrad_accumulate(int prec, void* acc, const void* slices, long long n,
                                     int splits, int first, cudaStream_t s);
+// Small-C (C <= 4, fp32 inputs, prec != FP64) weight gradient on the CUDA cores:
+// nblk blocks each write one M slice [16][K][m_ld] of `parts`; the slices are
+// summed into `summed` ([16][K][m_ld]).
+cudaError_t launch_wgrad_smallc(int prec, const void* d, const void* dy, void* parts,
+                                void* summed, int K, int C, int H, int W, int pad, int oh, int ow,
+                                int gh, int gw, long long B, long long m_ld, int nblk,
+                                cudaStream_t s);
 cudaError_t launch_wgrad_inverse(int prec, const void* Mbuf, void* dg, int K, int C,
                                  long long m_ld, int slices, cudaStream_t s);
 

@@ -1494,6 +1494,244 @@ __global__ void __launch_bounds__(256) wgrad_inverse_wide_kernel(const TA* __res
     for (int j = 0; j < 3; ++j) dst[i * 3 + j] = out[i][j];
 }
 
+// ---------------------------------------------- small-C weight gradient
+// C <= 4 (conv1.1): the tile-reduction GEMM would put 3 channels on the
+// tensor core's 128-row side (and stage 16 x K transformed dY values per tile
+// through HBM for 16 x C x K MACs).  Instead one pass on the CUDA cores reads
+// dY and d once: per group of 32 tiles the block stages the 2x2 dY patches of
+// 64 filters and the transformed input patches (B^T d B, C channels) in shared
+// memory, then thread (k, q) forms G y G^T for tiles q, q+4, ... and
+// accumulates the 16 x C products.  Operands are rounded to the GEMM operand
+// type first (products exact in fp32, as on the tensor core); fp32 is plain
+// FFMA (at least as accurate as 3xTF32).  Each block writes one M slice
+// [16][K][m_ld]; wgrad_reduce_slices_kernel sums them in a fixed order.
+template <int PREC>
+__device__ __forceinline__ float op_round(float x) {
+  if constexpr (PREC == kTF32) {
+    uint32_t b;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(x));
+    return __uint_as_float(b);
+  } else if constexpr (PREC == kBF16) {
+    return __bfloat162float(__float2bfloat16_rn(x));
+  } else if constexpr (PREC == kFP16) {
+    return __half2float(__float2half_rn(x));
+  } else {
+    return x;
+  }
+}
+
+constexpr int kWgSmallTiles = 32;  // tiles per staged group
+constexpr int kWgSmallK = 64;      // filters per block (grid.y covers K)
+
+template <int PREC, int CC>
+__global__ void __launch_bounds__(256) wgrad_smallc_kernel(
+    const float* __restrict__ d, const float* __restrict__ dy, float* __restrict__ Mparts, int K,
+    int H, int W, int pad, int oh, int ow, int gh, int gw, long long B, long long m_ld) {
+  constexpr int TG = kWgSmallTiles;
+  __shared__ float4 dyS[kWgSmallK][TG + 1];  // [k][tile] 2x2 dY patch
+  // [tile][comp * CC + c] transformed input; row stride VS float4s, picked so
+  // a quarter-warp's 8 loads (4 tiles x 2 component rows) hit distinct banks
+  constexpr int VS = CC == 1 ? 6 : CC == 2 ? 9 : CC == 3 ? 14 : 17;
+  __shared__ float4 vS[TG][VS];
+  griddep_launch();
+  griddep_wait();
+  const int tid = threadIdx.x;
+  // thread = (tile lane q, component row cq = xi, filter quad kq): filters
+  // 4kq..4kq+3 x components 4cq..4cq+3 x CC channels in registers, so every
+  // shared-memory value feeds 4 (V) or 4 CC (dY) multiply-adds
+  const int q = tid & 3, cq = (tid >> 2) & 3, kq = tid >> 4;
+  const int k0 = blockIdx.y * kWgSmallK;
+  const long long ngroups = (B + TG - 1) / TG;
+  const long long per_img = static_cast<long long>(gh) * gw;
+  // row cq of F(3,2)'s G = {1,0}, {1/2,1/2}, {1/2,-1/2}, {0,1}
+  const float g0 = cq == 0 ? 1.f : (cq == 3 ? 0.f : 0.5f);
+  const float g1 = cq == 0 ? 0.f : (cq == 1 ? 0.5f : (cq == 2 ? -0.5f : 1.f));
+  float acc[4][4][CC];  // [filter kk][component nu][channel]
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int c = 0; c < CC; ++c) acc[kk][i][c] = 0.f;
+
+  // this thread's dY element in every group: column j, row i of tile tl, for
+  // filters k0 + kd, k0 + kd + 2, ... (a warp reads 2 x 16 consecutive
+  // columns of one row); all 32 loads in flight at once
+  const int dj = tid & 1, dtl = (tid >> 1) & (TG - 1), di = (tid >> 6) & 1, kd = tid >> 7;
+  const long long kstride = 2LL * oh * ow;
+  for (long long g = blockIdx.x; g < ngroups; g += gridDim.x) {
+    const long long tb = g * TG;
+    {
+      const long long b = tb + dtl;
+      float v[kWgSmallK / 2];
+      if (b < B) {
+        const int n = static_cast<int>(b / per_img);
+        const int rem = static_cast<int>(b - n * per_img);
+        const int ty = rem / gw;
+        const int y = 2 * ty + di, x = 2 * (rem - ty * gw) + dj;
+        const bool ok = y < oh && x < ow;
+        const float* src = dy + ((static_cast<long long>(n) * K + k0 + kd) * oh + y) * ow + x;
+#pragma unroll
+        for (int it = 0; it < kWgSmallK / 2; ++it)
+          v[it] = (ok && k0 + kd + 2 * it < K) ? __ldg(src + it * kstride) : 0.f;
+      } else {
+#pragma unroll
+        for (int it = 0; it < kWgSmallK / 2; ++it) v[it] = 0.f;
+      }
+#pragma unroll
+      for (int it = 0; it < kWgSmallK / 2; ++it)
+        reinterpret_cast<float*>(&dyS[kd + 2 * it][dtl])[di * 2 + dj] = v[it];
+    }
+    // transformed input patches, one (tile, channel) per thread
+    if (tid < TG * CC) {
+      const int tl = tid % TG, c = tid / TG;
+      const long long b = tb + tl;
+      float out[4][4];
+      if (b < B) {
+        const int n = static_cast<int>(b / per_img);
+        const int rem = static_cast<int>(b - n * per_img);
+        const int ty = rem / gw;
+        const int y0 = 2 * ty - pad, x0 = 2 * (rem - ty * gw) - pad;
+        const float* plane = d + (static_cast<long long>(n) * CC + c) * H * W;
+        float in[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int yy = y0 + u, xx = x0 + v;
+            in[u][v] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? __ldg(plane + yy * W + xx) : 0.f;
+          }
+        sandwich<float, 4, 4>(in, out, [](int i2, int j2) { return Alg32::BT(i2, j2); });
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) out[u][v] = 0.f;
+      }
+      float* dst = reinterpret_cast<float*>(vS[tl]);  // row tl: [comp][c]
+#pragma unroll
+      for (int xi = 0; xi < 4; ++xi)
+#pragma unroll
+        for (int nu = 0; nu < 4; ++nu) dst[(xi * 4 + nu) * CC + c] = op_round<PREC>(out[xi][nu]);
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int t = q; t < TG; t += 4) {
+      float vv[4 * CC];  // V[4cq + nu][c]
+#pragma unroll
+      for (int i = 0; i < CC; ++i) {
+        const float4 f = vS[t][cq * CC + i];
+        vv[4 * i] = f.x;
+        vv[4 * i + 1] = f.y;
+        vv[4 * i + 2] = f.z;
+        vv[4 * i + 3] = f.w;
+      }
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const float4 y4 = dyS[4 * kq + kk][t];  // y[0][0], y[0][1], y[1][0], y[1][1]
+        // (G y G^T)[cq][nu]: row cq of G y, then the G^T columns
+        const float t0 = g0 * y4.x + g1 * y4.z, t1 = g0 * y4.y + g1 * y4.w;
+        const float u[4] = {t0, 0.5f * t0 + 0.5f * t1, 0.5f * t0 - 0.5f * t1, t1};
+#pragma unroll
+        for (int nu = 0; nu < 4; ++nu) {
+          const float uu = op_round<PREC>(u[nu]);
+#pragma unroll
+          for (int c = 0; c < CC; ++c)
+            acc[kk][nu][c] = fmaf(uu, vv[nu * CC + c], acc[kk][nu][c]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // fold the 4 tile lanes (fixed butterfly order), then lane q == 0 writes
+  // this block's slice
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int c = 0; c < CC; ++c) {
+        float v = acc[kk][i][c];
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        acc[kk][i][c] = v;
+      }
+  if (q != 0) return;
+  float* slice = Mparts + static_cast<size_t>(blockIdx.x) * 16 * K * m_ld;
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    const int k = k0 + 4 * kq + kk;
+    if (k >= K) break;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int c = 0; c < CC; ++c)
+        slice[(static_cast<size_t>(4 * cq + i) * K + k) * m_ld + c] = acc[kk][i][c];
+  }
+}
+
+// out[i] = sum over S slices of slices[s][i] (n elements each), in a fixed
+// order: block = 32 consecutive elements x 32 slice groups (coalesced rows,
+// ~S/32 loads in flight per thread), group sums folded in ascending order.
+__global__ void __launch_bounds__(1024) wgrad_reduce_slices_kernel(const float* __restrict__ sl,
+                                                                   float* __restrict__ out,
+                                                                   long long n, int S) {
+  griddep_launch();
+  griddep_wait();
+  __shared__ float part[32][33];
+  const int il = threadIdx.x & 31, sg = threadIdx.x >> 5;
+  const long long i = blockIdx.x * 32LL + il;
+  float v = 0.f;
+  if (i < n) {
+#pragma unroll 8
+    for (int s = sg; s < S; s += 32) v += sl[static_cast<size_t>(s) * n + i];
+  }
+  part[sg][il] = v;
+  __syncthreads();
+  if (sg != 0 || i >= n) return;
+  float r = part[0][il];
+#pragma unroll
+  for (int g2 = 1; g2 < 32; ++g2) r += part[g2][il];
+  out[i] = r;
+}
+
+template <int PREC>
+static cudaError_t wgrad_smallc_prec(const float* d, const float* dy, float* parts, int K, int C,
+                                     int H, int W, int pad, int oh, int ow, int gh, int gw,
+                                     long long B, long long m_ld, int nblk, cudaStream_t s) {
+  const dim3 grid(nblk, (K + kWgSmallK - 1) / kWgSmallK);
+  switch (C) {
+    case 1: launch_k(wgrad_smallc_kernel<PREC, 1>, grid, dim3(256), 0, s, d, dy, parts, K, H, W, pad, oh, ow, gh, gw, B, m_ld); break;
+    case 2: launch_k(wgrad_smallc_kernel<PREC, 2>, grid, dim3(256), 0, s, d, dy, parts, K, H, W, pad, oh, ow, gh, gw, B, m_ld); break;
+    case 3: launch_k(wgrad_smallc_kernel<PREC, 3>, grid, dim3(256), 0, s, d, dy, parts, K, H, W, pad, oh, ow, gh, gw, B, m_ld); break;
+    case 4: launch_k(wgrad_smallc_kernel<PREC, 4>, grid, dim3(256), 0, s, d, dy, parts, K, H, W, pad, oh, ow, gh, gw, B, m_ld); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wgrad_smallc(int prec, const void* d, const void* dy, void* parts,
+                                void* summed, int K, int C, int H, int W, int pad, int oh, int ow,
+                                int gh, int gw, long long B, long long m_ld, int nblk,
+                                cudaStream_t s) {
+  const float* df = static_cast<const float*>(d);
+  const float* yf = static_cast<const float*>(dy);
+  float* pf = static_cast<float*>(parts);
+  cudaError_t e;
+  switch (prec) {
+    case kFP32: e = wgrad_smallc_prec<kFP32>(df, yf, pf, K, C, H, W, pad, oh, ow, gh, gw, B, m_ld, nblk, s); break;
+    case kTF32: e = wgrad_smallc_prec<kTF32>(df, yf, pf, K, C, H, W, pad, oh, ow, gh, gw, B, m_ld, nblk, s); break;
+    case kBF16: e = wgrad_smallc_prec<kBF16>(df, yf, pf, K, C, H, W, pad, oh, ow, gh, gw, B, m_ld, nblk, s); break;
+    case kFP16: e = wgrad_smallc_prec<kFP16>(df, yf, pf, K, C, H, W, pad, oh, ow, gh, gw, B, m_ld, nblk, s); break;
+    default: return cudaErrorInvalidValue;
+  }
+  if (e != cudaSuccess) return e;
+  const long long n = 16LL * K * m_ld;
+  launch_k(wgrad_reduce_slices_kernel, dim3(static_cast<unsigned>((n + 31) / 32)), dim3(1024), 0,
+           s, static_cast<const float*>(parts), static_cast<float*>(summed), n, nblk);
+  return cudaGetLastError();
+}
+
 // acc (+)= sum_s slice[s], ascending s (one tile chunk's split partials).
 template <typename TA>
 __global__ void __launch_bounds__(256) wgrad_accumulate_kernel(TA* __restrict__ acc,
