@@ -910,8 +910,13 @@ int wgrad_plan(const wino_layer_t* layer, int prec, size_t limit, WgPlan* w) {
   w->nsplit = op_splits(prec);
   w->acc_bytes = prec == kFP64 ? 8 : 4;
   const size_t budget = limit ? limit : kWgradDefaultWorkspace;
+  size_t stage = budget;  // Uw + Vw bytes per tile chunk
+  if (const char* e = getenv("WINO_WGRAD_CHUNK_MB")) {  // tuning override
+    const size_t v = static_cast<size_t>(atoll(e)) << 20;
+    if (v > 0 && v < stage) stage = v;
+  }
   const size_t per_tile = static_cast<size_t>(w->nsplit) * 16 * (L.K + L.C) * w->esize;
-  long long nb = static_cast<long long>(budget / per_tile);
+  long long nb = static_cast<long long>(stage / per_tile);
   if (nb < 64) nb = 64;
   if (nb >= w->B) nb = w->B;
   else nb = nb / 64 * 64;
