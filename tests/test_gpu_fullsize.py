@@ -87,3 +87,26 @@ def test_linearity_conv42(wb):
     torch.cuda.synchronize()
     err = (yc - ya - yb).abs().max().item()
     assert err <= 1.5e-3, err
+
+
+@pytest.mark.parametrize("label,C,H,K,prec,tol", [
+    ("conv1.1", 3, 224, 64, "fp32", 1e-5),    # small-C CUDA-core pass
+    ("conv1.1", 3, 224, 64, "bf16", 2e-2),
+    # tensor-core GEMM with tile splits: 3xTF32 (measured 3.7e-5 at 200k-term sums)
+    ("conv1.2", 64, 224, 64, "fp32", 1e-4),
+    ("conv4.2", 512, 28, 512, "bf16", 2e-2),
+])
+def test_weight_gradient_full_size(wb, label, C, H, K, prec, tol):
+    """Weight gradient at VGG-E resolution (N = 4, every tile of the layer):
+    against torch's own weight gradient of the same correlation in fp64 on the
+    GPU (an independent algorithm), error relative to max|dg|."""
+    import torch
+    N = 4
+    cfg = wb.LayerConfig(N=N, C=C, H=H, W=H, K=K, pad=1)
+    gen = torch.Generator(device="cpu").manual_seed(C + K)
+    d = (torch.rand((N, C, H, H), generator=gen) * 2 - 1).cuda()
+    dy = (torch.rand((N, K, H, H), generator=gen) * 2 - 1).cuda()
+    got = wb.grad_weights_device(d, dy, cfg, prec).double()
+    ref = torch.nn.grad.conv2d_weight(d.double(), (K, C, 3, 3), dy.double(), padding=1)
+    err = ((got - ref).abs().max() / ref.abs().max()).item()
+    assert err <= tol, (label, prec, err)
