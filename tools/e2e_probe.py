@@ -49,6 +49,40 @@ def run(order, S, steps=5):
     return a.elapsed_time(b) / steps
 
 
+def run_split(steps=5):
+    """All H2D copies on one stream, all D2H copies on another; D2H of call i
+    waits for H2D of call i (stands in for the compute dependency)."""
+    hs, ds = torch.cuda.Stream(), torch.cuda.Stream()
+    bufs = [(torch.empty(i, pin_memory=True), torch.empty(i, device="cuda"),
+             torch.empty(o, device="cuda"), torch.empty(o, pin_memory=True))
+            for (_, i, o) in calls]
+
+    def step():
+        for hi, di, do, ho in bufs:
+            with torch.cuda.stream(hs):
+                di.copy_(hi, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(hs)
+            ds.wait_event(ev)
+            with torch.cuda.stream(ds):
+                ho.copy_(do, non_blocking=True)
+
+    step()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    cur = torch.cuda.current_stream()
+    a.record(cur)
+    hs.wait_stream(cur)
+    ds.wait_stream(cur)
+    for _ in range(steps):
+        step()
+    cur.wait_stream(hs)
+    cur.wait_stream(ds)
+    b.record(cur)
+    b.synchronize()
+    return a.elapsed_time(b) / steps
+
+
 nb_in = sum(i for _, i, _ in calls) * 4
 nb_out = sum(o for _, _, o in calls) * 4
 print(f"batch {B}: H2D {nb_in / 1e6:.1f} MB, D2H {nb_out / 1e6:.1f} MB per step")
@@ -59,3 +93,5 @@ for name, order in orders.items():
     for S in (2, 4, 8):
         ms = run(order, S)
         print(f"{name:12s} S={S}: {ms:.3f} ms/step  ({(nb_in + nb_out) / ms / 1e6:.1f} GB/s)")
+ms = run_split()
+print(f"split h2d/d2h streams: {ms:.3f} ms/step  ({(nb_in + nb_out) / ms / 1e6:.1f} GB/s)")
