@@ -956,7 +956,9 @@ int wgrad_plan(const wino_layer_t* layer, int prec, size_t limit, WgPlan* w) {
   }
   // C <= 4: the tensor-core GEMM would waste 125 of 128 rows and stage 16 x K
   // values per tile through HBM; the small-C kernel reads d and dY once
-  w->smallc = (L.C <= 4 && prec != kFP64 && !getenv("WINO_NO_WGRAD_SMALLC")) ? 1 : 0;
+  w->smallc = (L.C <= 4 && prec != kFP64 && w->B < (1LL << 31) - 64 &&
+               static_cast<long long>(w->oh) * w->ow * 2 < (1LL << 31) &&
+               !getenv("WINO_NO_WGRAD_SMALLC")) ? 1 : 0;
   if (w->smallc) {
     const long long groups = (w->B + 31) / 32;
     const int per_y = (2 * gemm_device_sms()) / ((L.K + 63) / 64);

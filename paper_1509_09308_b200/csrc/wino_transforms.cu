@@ -1541,8 +1541,11 @@ __global__ void __launch_bounds__(256) wgrad_smallc_kernel(
   // shared-memory value feeds 4 (V) or 4 CC (dY) multiply-adds
   const int q = tid & 3, cq = (tid >> 2) & 3, kq = tid >> 4;
   const int k0 = blockIdx.y * kWgSmallK;
-  const long long ngroups = (B + TG - 1) / TG;
-  const long long per_img = static_cast<long long>(gh) * gw;
+  // tile indices fit in 32 bits (the planner checks B < 2^31): 32-bit
+  // division and offsets keep the load phase short
+  const int Bi = static_cast<int>(B);
+  const int ngroups = (Bi + TG - 1) / TG;
+  const int per_img = gh * gw;
   // row cq of F(3,2)'s G = {1,0}, {1/2,1/2}, {1/2,-1/2}, {0,1}
   const float g0 = cq == 0 ? 1.f : (cq == 3 ? 0.f : 0.5f);
   const float g1 = cq == 0 ? 0.f : (cq == 1 ? 0.5f : (cq == 2 ? -0.5f : 1.f));
@@ -1558,22 +1561,32 @@ __global__ void __launch_bounds__(256) wgrad_smallc_kernel(
   // filters k0 + kd, k0 + kd + 2, ... (a warp reads 2 x 16 consecutive
   // columns of one row); all 32 loads in flight at once
   const int dj = tid & 1, dtl = (tid >> 1) & (TG - 1), di = (tid >> 6) & 1, kd = tid >> 7;
-  const long long kstride = 2LL * oh * ow;
-  for (long long g = blockIdx.x; g < ngroups; g += gridDim.x) {
-    const long long tb = g * TG;
+  const int kstride = 2 * oh * ow;  // two filter planes
+  // loads with k = k0 + kd + 2 it < K
+  const int nit = min(kWgSmallK / 2, (K - k0 - kd + 1) / 2);
+  for (int g = blockIdx.x; g < ngroups; g += gridDim.x) {
+    const int tb = g * TG;
     {
-      const long long b = tb + dtl;
+      const int b = tb + dtl;
       float v[kWgSmallK / 2];
-      if (b < B) {
-        const int n = static_cast<int>(b / per_img);
-        const int rem = static_cast<int>(b - n * per_img);
+      int n = 0, y = oh, x = 0;
+      if (b < Bi) {
+        n = b / per_img;
+        const int rem = b - n * per_img;
         const int ty = rem / gw;
-        const int y = 2 * ty + di, x = 2 * (rem - ty * gw) + dj;
-        const bool ok = y < oh && x < ow;
+        y = 2 * ty + di;
+        x = 2 * (rem - ty * gw) + dj;
+      }
+      if (y < oh && x < ow) {
         const float* src = dy + ((static_cast<long long>(n) * K + k0 + kd) * oh + y) * ow + x;
+        if (nit == kWgSmallK / 2) {  // all 64 filters of the block exist
 #pragma unroll
-        for (int it = 0; it < kWgSmallK / 2; ++it)
-          v[it] = (ok && k0 + kd + 2 * it < K) ? __ldg(src + it * kstride) : 0.f;
+          for (int it = 0; it < kWgSmallK / 2; ++it) v[it] = __ldg(src + it * kstride);
+        } else {
+#pragma unroll
+          for (int it = 0; it < kWgSmallK / 2; ++it)
+            v[it] = it < nit ? __ldg(src + it * kstride) : 0.f;
+        }
       } else {
 #pragma unroll
         for (int it = 0; it < kWgSmallK / 2; ++it) v[it] = 0.f;
@@ -1585,11 +1598,11 @@ __global__ void __launch_bounds__(256) wgrad_smallc_kernel(
     // transformed input patches, one (tile, channel) per thread
     if (tid < TG * CC) {
       const int tl = tid % TG, c = tid / TG;
-      const long long b = tb + tl;
+      const int b = tb + tl;
       float out[4][4];
-      if (b < B) {
-        const int n = static_cast<int>(b / per_img);
-        const int rem = static_cast<int>(b - n * per_img);
+      if (b < Bi) {
+        const int n = b / per_img;
+        const int rem = b - n * per_img;
         const int ty = rem / gw;
         const int y0 = 2 * ty - pad, x0 = 2 * (rem - ty * gw) - pad;
         const float* plane = d + (static_cast<long long>(n) * CC + c) * H * W;
