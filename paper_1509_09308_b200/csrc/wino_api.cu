@@ -957,7 +957,7 @@ int wgrad_plan(const wino_layer_t* layer, int prec, size_t limit, WgPlan* w) {
   // C <= 4: the tensor-core GEMM would waste 125 of 128 rows and stage 16 x K
   // values per tile through HBM; the small-C kernel reads d and dY once
   w->smallc = (L.C <= 4 && prec != kFP64 && w->B < (1LL << 31) - 64 &&
-               static_cast<long long>(w->oh) * w->ow * 2 < (1LL << 31) &&
+               static_cast<long long>(w->oh) * w->ow * 64 < (1LL << 31) &&  // 32-bit load offsets
                !getenv("WINO_NO_WGRAD_SMALLC")) ? 1 : 0;
   if (w->smallc) {
     const long long groups = (w->B + 31) / 32;
