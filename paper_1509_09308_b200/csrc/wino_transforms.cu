@@ -83,17 +83,19 @@ __device__ __forceinline__ void filter_block(const typename OpStore<PREC>::T* __
   if (nloc == NP && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
     constexpr int NVT = NP * 9 / VE;           // 16-byte chunks in the block (NP % 4 == 0)
     constexpr int NV = (NVT + 255) / 256;      // per thread, all in flight
-    uint4 v[NV];
+    // cp.async straight into shared memory: every chunk's load is in flight at
+    // once (register staging let the compiler interleave loads and stores,
+    // i.e. several dependent round trips)
+    const uint32_t s0 = static_cast<uint32_t>(__cvta_generic_to_shared(sg));
 #pragma unroll
     for (int q = 0; q < NV; ++q) {
       const int i = threadIdx.x + 256 * q;
-      if (NVT % 256 == 0 || i < NVT) v[q] = __ldg(reinterpret_cast<const uint4*>(src) + i);
+      if (NVT % 256 == 0 || i < NVT)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s0 + 16 * i),
+                     "l"(reinterpret_cast<const uint4*>(src) + i)
+                     : "memory");
     }
-#pragma unroll
-    for (int q = 0; q < NV; ++q) {
-      const int i = threadIdx.x + 256 * q;
-      if (NVT % 256 == 0 || i < NVT) reinterpret_cast<uint4*>(sg)[i] = v[q];
-    }
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
   } else {
     for (int e = threadIdx.x; e < nloc * 9; e += 256) sg[e] = __ldg(src + e);
   }
