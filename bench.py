@@ -215,7 +215,7 @@ def run_reference_arm(args) -> None:
     if rank != 0:
         return
     m, fx = (2 if args.algo.startswith("f2x2") else 4), args.algo.endswith("-fx")
-    batch = args.batch * world
+    batch = args.global_batch if args.global_batch > 0 else args.batch * world
     use_ref = _ref_available()
     cores = _cpu_threads()
     cpu_reference_pass(1, m, fx, use_ref, layers=(("warm", 3, 8, 4, 1),))
@@ -271,13 +271,28 @@ def run_gpu(args) -> None:
         dist.init_process_group("nccl", device_id=dev)
     m, fx, prec = wb.parse_algo(args.algo)
     prec = args.prec or prec or "fp32"
-    B = args.batch  # images per GPU (weak scaling: per-GPU work fixed)
+    strong = args.global_batch > 0
+    if strong:
+        # strong scaling (config 4): a fixed global batch split contiguously over
+        # the ranks by the batch-shard driver (sharding.ShardedForward)
+        from paper_1509_09308_b200 import sharding
+        _, B = sharding.shard_bounds(args.global_batch, world, rank)
+        if B < 1:
+            raise SystemExit(f"--global-batch {args.global_batch} leaves rank {rank} empty")
+    else:
+        B = args.batch  # images per GPU (weak scaling: per-GPU work fixed)
     gen = torch.Generator(device="cpu").manual_seed(1234 + rank)
 
     layers = []
     for i, (lbl, C, H, K, depth) in enumerate(VGG_E):
-        cfg = wb.LayerConfig(N=B, C=C, H=H, W=H, K=K, pad=1)
-        plan = weng.WinogradPlan(cfg, m, prec, workspace_limit=args.workspace)
+        if strong:
+            gcfg = wb.LayerConfig(N=args.global_batch, C=C, H=H, W=H, K=K, pad=1)
+            shard = sharding.ShardedForward(gcfg, m, prec, world, rank,
+                                            workspace_limit=args.workspace)
+            cfg, plan = shard.cfg, shard.plan
+        else:
+            cfg = wb.LayerConfig(N=B, C=C, H=H, W=H, K=K, pad=1)
+            plan = weng.WinogradPlan(cfg, m, prec, workspace_limit=args.workspace)
         # synthetic U[-1,1) data (this rank's shard) and replicated filters
         d_host = (torch.rand((B, C, H, H), generator=gen) * 2 - 1).pin_memory()
         g_host = torch.rand((K, C, 3, 3), generator=torch.Generator().manual_seed(i)) * 2 - 1
@@ -287,10 +302,19 @@ def run_gpu(args) -> None:
         y_host = torch.empty(plan.out_shape, dtype=torch.float32).pin_memory()
         ws = plan.alloc_workspace(dev)
         U = plan.filter_transform(g) if fx else None
+        if strong and fx:
+            shard.set_filters(g)
+            U = shard.U
         layers.append(dict(lbl=lbl, C=C, H=H, K=K, depth=depth, cfg=cfg, plan=plan, d=d, g=g,
+                           shard=shard if strong else None,
                            y=y, ws=ws, U=U, d_host=d_host, y_host=y_host,
                            gf=gflop_direct(B, C, H, K)))
-    gf_step = sum(L["gf"] * L["depth"] for L in layers)
+    gf_step = sum(L["gf"] * L["depth"] for L in layers)  # this rank's share
+    # whole-job GFLOP per step: every rank's shard (weak: world x B images;
+    # strong: the fixed global batch)
+    gf_job = (sum(gflop_direct(args.global_batch, C, H, K) * dep for (_, C, H, K, dep) in VGG_E)
+              if strong else gf_step * world)
+    images_job = args.global_batch if strong else B * world
     launches_step = sum(L["depth"] * (L["plan"].info["launches_per_forward"] +
                                       (0 if fx or L["plan"].info["combined_transforms"] else 1))
                         for L in layers)
@@ -300,8 +324,12 @@ def run_gpu(args) -> None:
     def step_body(s):
         for L in layers:
             for _ in range(L["depth"]):
-                L["plan"].forward(L["d"], y=L["y"], U=L["U"], g=None if fx else L["g"],
-                                  workspace=L["ws"], stream=s)
+                if L["shard"] is not None:  # batch-shard driver (strong scaling)
+                    L["shard"].forward(L["d"], y_local=L["y"], workspace=L["ws"], stream=s,
+                                       g=None if fx else L["g"])
+                else:
+                    L["plan"].forward(L["d"], y=L["y"], U=L["U"], g=None if fx else L["g"],
+                                      workspace=L["ws"], stream=s)
 
     # capture the whole step in one CUDA graph (launch-bound at N=1)
     with torch.cuda.stream(stream):
@@ -355,9 +383,9 @@ def run_gpu(args) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_max = float(t.item())
     ms_per_step = t_max / args.steps * 1e3
-    total_gf = gf_step * world * args.steps
+    total_gf = gf_job * args.steps
     value = total_gf / t_max / 1e3  # TFLOPS, whole job
-    images_per_s = B * world * args.steps / t_max
+    images_per_s = images_job * args.steps / t_max
 
     # ---- live per-stage kernel timing (CUDA events on the launch stream)
     stage_bytes = [0.0] * 4  # algorithmic HBM bytes
@@ -467,27 +495,31 @@ def run_gpu(args) -> None:
     te = torch.tensor([ea.elapsed_time(eb) / 1e3], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_val = gf_step * world * e2e_steps / float(te.item()) / 1e3
+    e2e_val = gf_job * e2e_steps / float(te.item()) / 1e3
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(1, m, fx, budget_s=args.cpu_budget)
 
     if rank == 0:
-        pub = PUBLISHED_F2.get(prec, {}).get(B * world) if (m == 2 and not fx) else None
+        pub = PUBLISHED_F2.get(prec, {}).get(images_job) if (m == 2 and not fx) else None
         clocks = sampler.summary()
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOPS",
             "images_per_s": images_per_s, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": (value / pub) if pub else None,
+            "scaling": "strong" if strong else "weak", "vs_baseline": (value / pub) if pub else None,
             "vs_baseline_ref": ("paper F(2x2) VGG-E Titan X, PAPER.md:565-607" if pub else None),
             "dtype": prec, "data": "synthetic",
             "config": {"workload": f"VGG-E 16 conv layers (9 shapes, depth-weighted), "
                                    f"{args.algo} F({m}x{m},3x3), GEMM {prec}"
-                                   f"{' (3xTF32)' if prec == 'fp32' else ''}, N={B} per GPU",
-                       "algo": args.algo, "global_batch": B * world, "batch_per_gpu": B,
-                       "parallelism": f"dp{world} batch-shard (no collective)",
+                                   f"{' (3xTF32)' if prec == 'fp32' else ''}, "
+                                   + (f"global N={args.global_batch} split over {world} GPU(s)"
+                                      if strong else f"N={B} per GPU"),
+                       "algo": args.algo, "global_batch": images_job, "batch_per_gpu": B,
+                       "parallelism": f"dp{world} batch-shard (no collective)"
+                                      + (", sharding.ShardedForward" if strong else ""),
+                       "workspace_limit": args.workspace,
                        "l2": f"flushed between timed steps ({args.flush_mb} MB write)",
                        "cuda_graph": graph is not None},
             "roofline": roof,
@@ -513,7 +545,12 @@ def main() -> None:
     ap.add_argument("--algo", default="f2x2")
     ap.add_argument("--prec", default=None, choices=(None, "fp32", "tf32", "bf16", "fp16"))
     ap.add_argument("--batch", type=int, default=1, help="images per GPU")
-    ap.add_argument("--workspace", type=int, default=0, help="chunk budget bytes (0 = auto)")
+    ap.add_argument("--workspace", type=int, default=0,
+                    help="transform-space staging budget in bytes (0 = planner default 128 MiB; "
+                         "16777216 = the paper's 16 MB)")
+    ap.add_argument("--global-batch", type=int, default=0,
+                    help="strong scaling: this global N is split over the ranks "
+                         "(default: --batch images per GPU, weak scaling)")
     ap.add_argument("--flush-mb", type=int, default=256)
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -19,8 +19,10 @@
  *   WINO_ECUDA        4  -> RuntimeError
  *
  * Thread-safety: plans are immutable after creation; every call is reentrant
- * across host threads and streams (no global mutable state besides the
- * thread-local error string and a once-initialised driver entry point).
+ * across host threads and streams.  Global state: the thread-local error
+ * string, a once-initialised driver entry point, and per-(kernel, device)
+ * "attributes set" flags and SM counts (atomics; setting them is idempotent),
+ * so one process may drive several GPUs (cudaSetDevice before each call).
  */
 #ifndef WINO_H_
 #define WINO_H_
@@ -75,12 +77,18 @@ typedef struct {
   int fused_splits;           /* split-C factor of the fused kernel              */
   int m_bytes_per_elem;       /* staged M element: 4 (fp32), 2 (bf16 GEMM), 8   */
   int combined_transforms;    /* non-FX forwards launch filter+input together   */
+  size_t staging_bytes;       /* transform-space staging (V + M of the chunks in
+                                 flight): all an FX forward (U passed) needs;
+                                 <= workspace_limit when one is given            */
 } wino_plan_info_t;
 
 /* Create a plan.  m in {2,4} (F(2x2,3x3), F(4x4,3x3)); R == S == 3.
- * workspace_limit: byte budget for the per-chunk V+M staging buffers
- * (0 = default, sized to stay L2-resident).  The tile/workspace planner splits
- * the tile grid into row chunks that fit the budget. */
+ * workspace_limit: hard cap in bytes on the transform-space staging (V + M of
+ * the chunks in flight; see staging_bytes).  0 = default budget of 128 MiB,
+ * sized to stay L2-resident.  The tile/workspace planner splits the tile grid
+ * into row chunks that fit and reduces split-C when its partial sums would
+ * not; 16 MiB is the paper's workspace bound.  A limit
+ * smaller than one tile row's staging still plans one row per chunk. */
 int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspace_limit,
                      wino_plan_t* out);
 int wino_plan_destroy(wino_plan_t plan);
@@ -96,7 +104,7 @@ int wino_filter_transform(wino_plan_t plan, const void* g, void* U, void* stream
  * U: precomputed wino_filter_transform output, or NULL to transform g here
  *    (g must then be non-NULL; the U stack lives in the workspace).
  * y: (N,K,out_h,out_w) output, fully written (every element).
- * workspace: >= info.workspace_bytes (U==NULL) or >= workspace_bytes-u_bytes. */
+ * workspace: >= info.workspace_bytes (U==NULL) or >= info.staging_bytes (U given). */
 int wino_forward(wino_plan_t plan, const void* d, const void* U, const void* g, void* y,
                  void* workspace, size_t workspace_bytes, void* stream);
 

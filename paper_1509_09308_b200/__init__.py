@@ -17,7 +17,7 @@ from .layer import LayerConfig, OpCounter, WinogradAlgorithm, builtin, builtin_s
 from .suites import LayerSuite, get_suite, vgg_e, vgg_e_accuracy
 from .tensors import Precision, Tensor4, fill_uniform, max_abs_error, quantize_fp16
 
-__version__ = "0.1.0"
+__version__ = "0.2.0"
 
 __all__ = [
     "Precision", "Tensor4", "fill_uniform", "quantize_fp16", "max_abs_error",

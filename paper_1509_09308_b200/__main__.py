@@ -43,13 +43,16 @@ def build_parser() -> argparse.ArgumentParser:
 
 def main(argv: Optional[list] = None) -> int:
     args = build_parser().parse_args(argv)
-    from .commands import cmd_accuracy, cmd_bench, parse_algo
+    from .commands import BENCH_ALGOS, WINOGRAD_ALGOS, cmd_accuracy, cmd_bench
     try:
         if args.command == "accuracy":
             rep = cmd_accuracy(suite=args.suite, algos=[a for a in args.algos.split(",") if a],
                                precision=args.precision, seed=args.seed, scale=args.scale)
         else:
-            parse_algo(args.algo)
+            if (args.algo not in BENCH_ALGOS
+                    and args.algo.partition(":")[0] not in WINOGRAD_ALGOS):
+                raise ValueError(f"unknown algorithm {args.algo!r}; known: "
+                                 f"{', '.join(BENCH_ALGOS)}")
             if args.batch < 1:
                 raise ValueError(f"batch must be >= 1, got {args.batch}")
             rep = cmd_bench(suite=args.suite, algo=args.algo, batch=args.batch,

@@ -50,6 +50,7 @@ class PlanInfo(ctypes.Structure):
         ("multiplies", ctypes.c_longlong),
         ("fused", ctypes.c_int), ("fused_splits", ctypes.c_int),
         ("m_bytes_per_elem", ctypes.c_int), ("combined_transforms", ctypes.c_int),
+        ("staging_bytes", ctypes.c_size_t),
     ]
 
     def as_dict(self) -> dict:

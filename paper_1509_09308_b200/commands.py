@@ -17,8 +17,10 @@ from .layer import LayerConfig, builtin, gflops_direct
 from .suites import get_suite
 from .tensors import Precision, Tensor4, fill_uniform, max_abs_error, quantize_fp16
 
-BENCH_ALGOS = ("f2x2", "f4x4", "f2x2-fx", "f4x4-fx")
+WINOGRAD_ALGOS = ("f2x2", "f4x4", "f2x2-fx", "f4x4-fx")
 DIRECT_ALGOS = ("direct", "direct-fp32")
+BENCH_ALGOS = ("direct", "direct-fp32", "f2x2", "f4x4", "f2x2-fx", "f4x4-fx",
+               "fft")  # commands.py:26
 ACCURACY_ALGOS = ("direct-fp32", "f2x2", "f4x4", "fft")  # commands.py:25
 PRECISIONS = ("fp32", "tf32", "bf16", "fp16", "fp64")
 
@@ -26,8 +28,8 @@ PRECISIONS = ("fp32", "tf32", "bf16", "fp16", "fp64")
 def parse_algo(algo: str) -> Tuple[int, bool, Optional[str]]:
     """'f4x4-fx:bf16' -> (m=4, fx=True, prec='bf16')."""
     base, _, prec = algo.partition(":")
-    if base not in BENCH_ALGOS:
-        raise ValueError(f"unknown algorithm {algo!r}; known: {', '.join(BENCH_ALGOS)}"
+    if base not in WINOGRAD_ALGOS:
+        raise ValueError(f"unknown algorithm {algo!r}; known: {', '.join(WINOGRAD_ALGOS)}"
                          " (optionally ':<prec>')")
     if prec and prec not in PRECISIONS:
         raise ValueError(f"unknown precision {prec!r}; known: {', '.join(PRECISIONS)}")
@@ -91,16 +93,42 @@ class Report:
         return "\n".join(out) + "\n"
 
 
+def _bench_other(algo: str, cfg: LayerConfig, d: Tensor4, g: Tensor4, repeats: int) -> float:
+    """Best-of-N seconds of the non-Winograd algorithms (direct, direct-fp32, fft)
+    through run_layer -- host Tensor4 in and out, like the reference's timing of
+    them (commands.py:160-166): wall clock around a synchronised call."""
+    import time
+
+    import torch
+    run_layer(algo, d, g, cfg)  # warm-up, untimed
+    best = float("inf")
+    for _ in range(repeats):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        run_layer(algo, d, g, cfg)
+        torch.cuda.synchronize()
+        best = min(best, time.perf_counter() - t0)
+    return best
+
+
 def cmd_bench(suite: str = "vgg-e", algo: str = "f2x2", batch: int = 1, repeats: int = 3,
               scale: float = 1.0, seed: int = 0) -> Report:
-    """Per-layer best-of-N device time (CUDA events) and effective GFLOPS
-    = direct-conv GFLOP / time; depth-weighted TOTAL row (commands.py:136-178).
-    Inputs are resident in HBM; non-FX algorithms include the filter transform."""
+    """Per-layer best-of-N time and effective GFLOPS = direct-conv GFLOP / time;
+    depth-weighted TOTAL row (commands.py:136-178).  Every reference algorithm
+    name is accepted (BENCH_ALGOS, commands.py:26).  The Winograd names are
+    device-timed (CUDA events, inputs resident in HBM, non-FX names include
+    the filter transform); direct / direct-fp32 / fft are timed through
+    run_layer around a synchronised call.  Layers that exhaust memory are skipped
+    with empty cells."""
     import torch
 
     if repeats < 1:
         raise ValueError(f"repeats must be >= 1, got {repeats}")
-    m, fx, prec = parse_algo(algo)
+    if algo not in BENCH_ALGOS and algo.partition(":")[0] not in WINOGRAD_ALGOS:
+        raise ValueError(f"unknown algorithm {algo!r}; known: {', '.join(BENCH_ALGOS)}")
+    wino = algo.partition(":")[0] in WINOGRAD_ALGOS
+    if wino:
+        m, fx, prec = parse_algo(algo)
     layers = get_suite(suite).scaled(scale).with_batch(batch)
     rep = Report(columns=("layer", "algo", "batch", "msec", "effective_gflops"), seed=seed)
     total_sec = total_gf = 0.0
@@ -108,26 +136,30 @@ def cmd_bench(suite: str = "vgg-e", algo: str = "f2x2", batch: int = 1, repeats:
         cfg = entry.cfg
         try:
             d, g = layer_inputs(cfg, seed, i)
-            plan = get_plan(cfg, m, prec or "fp32")
-            d_dev = torch.from_numpy(d.data.copy()).cuda()
-            g_dev = torch.from_numpy(g.data.copy()).cuda()
-            ws = plan.alloc_workspace()
-            y = torch.empty(plan.out_shape, dtype=plan.data_dtype, device="cuda")
-            U = plan.filter_transform(g_dev) if fx else None
+            if not wino:
+                best = _bench_other(algo, cfg, d, g, repeats)
+            else:
+                plan = get_plan(cfg, m, prec or "fp32")
+                d_dev = torch.from_numpy(d.data.copy()).cuda()
+                g_dev = torch.from_numpy(g.data.copy()).cuda()
+                ws = plan.alloc_workspace()
+                y = torch.empty(plan.out_shape, dtype=plan.data_dtype, device="cuda")
+                U = plan.filter_transform(g_dev) if fx else None
 
-            def step():
-                plan.forward(d_dev, y=y, U=U, g=None if fx else g_dev, workspace=ws)
+                def step():
+                    plan.forward(d_dev, y=y, U=U, g=None if fx else g_dev, workspace=ws)
 
-            step()  # warm-up, untimed
-            best = float("inf")
-            for _ in range(repeats):
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                torch.cuda.synchronize()
-                a.record()
-                step()
-                b.record()
-                b.synchronize()
-                best = min(best, a.elapsed_time(b) / 1e3)
+                step()  # warm-up, untimed
+                best = float("inf")
+                for _ in range(repeats):
+                    a = torch.cuda.Event(enable_timing=True)
+                    b = torch.cuda.Event(enable_timing=True)
+                    torch.cuda.synchronize()
+                    a.record()
+                    step()
+                    b.record()
+                    b.synchronize()
+                    best = min(best, a.elapsed_time(b) / 1e3)
         except (MemoryError, torch.cuda.OutOfMemoryError):
             rep.add(entry.label, algo, batch, None, None)
             continue
@@ -149,7 +181,7 @@ def cmd_accuracy(suite: str = "vgg-e-accuracy", algos: Sequence[str] = ACCURACY_
         raise ValueError(f"precision must be fp32 or fp16, got {precision!r}")
     for a in algos:
         base = a.partition(":")[0]
-        if a not in ACCURACY_ALGOS and a not in DIRECT_ALGOS and base not in BENCH_ALGOS:
+        if a not in ACCURACY_ALGOS and a not in DIRECT_ALGOS and base not in WINOGRAD_ALGOS:
             raise ValueError(f"unknown algorithm {a!r}; known: {', '.join(ACCURACY_ALGOS)}")
     layers = get_suite(suite).scaled(scale)
     tag = "fp32" if precision == "fp32" else Precision.FP16_SIM.value

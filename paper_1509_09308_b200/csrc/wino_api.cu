@@ -36,6 +36,7 @@ struct wino_plan_s {
   size_t u_bytes, v_bytes, m_bytes;  // v/m per full chunk
   int u_split2;                      // non-FX 3xTF32 staged: U as hi/lo planes in the workspace
   size_t u_ws;                       // workspace bytes of a forward-computed U
+  size_t staging_bytes;              // V + M of the chunks in flight (+ fused partials)
 };
 
 namespace wino {
@@ -195,6 +196,8 @@ static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // Default chunk budget: transform-space staging that stays L2-resident.
 constexpr size_t kDefaultWorkspace = 128ull << 20;
+// The staged input-transform kernels put a chunk's tile rows on grid.y.
+constexpr long long kMaxChunkRows = 65535;
 
 }  // namespace wino
 
@@ -204,7 +207,11 @@ extern "C" {
 
 const char* wino_last_error(void) { return g_err.c_str(); }
 
-const char* wino_version(void) { return "wino-b200 0.1.0 (sm_100a)"; }
+#ifndef WINO_SRC_HASH
+#define WINO_SRC_HASH "unknown000000000"
+#endif
+// The source hash lets build() detect a stale library (build.py).
+const char* wino_version(void) { return "wino-b200 0.2.0 (sm_100a) src " WINO_SRC_HASH; }
 
 int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspace_limit,
                      wino_plan_t* out) {
@@ -297,6 +304,7 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
   long long rows = static_cast<long long>(budget / (per_row ? per_row : 1));
   if (rows < 1) rows = 1;
   if (rows > p->rows_total) rows = p->rows_total;
+  if (rows > kMaxChunkRows) rows = kMaxChunkRows;
   p->rows_per_chunk = static_cast<int>(rows);
   p->num_chunks = (p->rows_total + p->rows_per_chunk - 1) / p->rows_per_chunk;
   p->chunk_tiles = static_cast<long long>(p->rows_per_chunk) * p->tw;
@@ -373,6 +381,7 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
       long long r2 = static_cast<long long>(budget / (per_row_v ? per_row_v : 1));
       if (r2 < 1) r2 = 1;
       if (r2 > p->rows_total) r2 = p->rows_total;
+      if (r2 > kMaxChunkRows) r2 = kMaxChunkRows;
       p->rows_per_chunk = static_cast<int>(r2);
       p->num_chunks = (p->rows_total + p->rows_per_chunk - 1) / p->rows_per_chunk;
       p->chunk_tiles = static_cast<long long>(p->rows_per_chunk) * p->tw;
@@ -409,6 +418,7 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
     p->nbuf = ns;
     long long r2 = static_cast<long long>((budget / ns) / (per_row ? per_row : 1));
     if (r2 < 1) r2 = 1;
+    if (r2 > kMaxChunkRows) r2 = kMaxChunkRows;
     p->rows_per_chunk = static_cast<int>(r2);
     p->num_chunks = (p->rows_total + p->rows_per_chunk - 1) / p->rows_per_chunk;
     p->chunk_tiles = static_cast<long long>(p->rows_per_chunk) * p->tw;
@@ -430,10 +440,32 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
                  gemm_tmem_a_enabled() && (p->P + 127) / 128 >= 16 &&
                  getenv("WINO_NO_USPLIT") == nullptr) ? 1 : 0;
   p->u_ws = p->u_split2 ? 2 * p->u_bytes : p->u_bytes;
-  p->m_bytes = (p->smallc || p->path != kPathStaged) ? 0
-                        : align_up(static_cast<size_t>(p->splits) * p->a2 * L.K * p->m_ld *
-                                       p->m_es,
-                                   1024);
+  auto set_m_bytes = [&] {
+    p->m_bytes = (p->smallc || p->path != kPathStaged) ? 0
+                          : align_up(static_cast<size_t>(p->splits) * p->a2 * L.K * p->m_ld *
+                                         p->m_es,
+                                     1024);
+  };
+  set_m_bytes();
+  // An explicit workspace_limit is a hard cap on the transform-space staging
+  // (V + M of every chunk in flight, + fused split-C partials; U excluded -- it
+  // is the FX filter workspace, or the caller passes it).  The chunk planner
+  // sized V + M for one split; split-C multiplies M, so it is reduced here until
+  // the staging fits (the paper's <= 16 MB mode).
+  if (workspace_limit) {
+    const int num_kb = gemm_num_kblocks(prec, L.C);
+    while (p->splits > 1 && p->nbuf * (p->v_bytes + p->m_bytes) + p->ypart_bytes > workspace_limit) {
+      const int kbps = (num_kb + p->splits - 2) / (p->splits - 1);
+      p->splits = (num_kb + kbps - 1) / kbps;
+      if (p->splits == 1 && prec == kBF16 && getenv("WINO_M_FP32") == nullptr && !p->smallc &&
+          p->path == kPathStaged) {
+        p->m_es = 2;
+        p->m_bf16 = 1;
+      }
+      set_m_bytes();
+    }
+  }
+  p->staging_bytes = p->nbuf * (p->v_bytes + p->m_bytes) + p->ypart_bytes;
   *out = p;
   return WINO_OK;
 }
@@ -485,6 +517,7 @@ int wino_plan_get_info(wino_plan_t p, wino_plan_info_t* info) {
   info->fused_splits = p->fsplits;
   info->m_bytes_per_elem = p->m_es;
   info->combined_transforms = plan_combines_transforms(p) ? 1 : 0;
+  info->staging_bytes = p->staging_bytes;
   info->fused_small_c = p->smallc ? 1 : 0;
   info->multiplies = p->P * p->L.C * static_cast<long long>(p->L.K) * p->a2;
   return WINO_OK;

@@ -40,6 +40,10 @@ __global__ void __launch_bounds__(256) direct_conv_kernel(const TI* __restrict__
                                                           TA* __restrict__ y, int N, int C, int H,
                                                           int W, int K, int R, int S, int pad,
                                                           int oh, int ow) {
+  // launched with PDL like every library kernel: wait for the predecessor's
+  // writes (d may be the output of the previous launch on this stream)
+  griddep_wait();
+  griddep_launch();
   const long long o = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const long long total = static_cast<long long>(N) * K * oh * ow;
   if (o >= total) return;

@@ -645,12 +645,12 @@ static cudaError_t launch_fused_t(const FusedArgs& f, cudaStream_t s) {
     tmV = tmU;  // unused
   }
   auto kern = wfused_kernel<M, PREC, VT>;
-  static bool configured = false;
-  if (!configured) {
+  static DeviceOnce configured;
+  if (configured.first()) {
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::smem);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured.done();
   }
   const int splits = f.splits < 1 ? 1 : f.splits;
   const int num_kb = (f.C + Cf::bkc - 1) / Cf::bkc;
@@ -687,9 +687,9 @@ static cudaError_t launch_fused_t(const FusedArgs& f, cudaStream_t s) {
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  static bool reported = false;  // WINO_DEBUG=1: report cluster occupancy once per variant
-  if (!reported) {
-    reported = true;
+  static DeviceOnce reported;
+  if (reported.first()) {
+    reported.done();
     const char* dbg = getenv("WINO_DEBUG");
     if (dbg && dbg[0] == '1') {
       int ncl = -1;

@@ -644,13 +644,13 @@ static cudaError_t launch_tc2(const GemmArgs& a, cudaStream_t s) {
                       static_cast<uint64_t>(a.K) * a.m_ld * 4ull, 32, 32))
     return cudaErrorInvalidValue;
   auto kern = wgemm_tc2_kernel<BN, BS>;
-  static bool configured = false;
-  if (!configured) {
+  static DeviceOnce configured;
+  if (configured.first()) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, total);
     if (e != cudaSuccess) return e;
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
-    configured = true;
+    configured.done();
   }
   const int num_kb = (a.C + Tr::bk - 1) / Tr::bk;
   const int kbps = (num_kb + splits - 1) / splits;
@@ -736,13 +736,18 @@ __global__ void __launch_bounds__(256) wgemm_f64_kernel(const double* __restrict
 }
 
 // ------------------------------------------------------------ launch
-static int num_sms() {
-  static int n = 0;  // benign race: idempotent
+static int num_sms() { return device_sms(); }
+
+int device_sms() {
+  static std::atomic<int> cache[64];  // per device; benign race (idempotent)
+  const int b = DeviceOnce::bit();
+  int n = cache[b].load(std::memory_order_relaxed);
   if (n == 0) {
     int dev = 0, v = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
     n = v > 0 ? v : 148;
+    cache[b].store(n, std::memory_order_relaxed);
   }
   return n;
 }
@@ -776,14 +781,14 @@ static cudaError_t launch_tc(const GemmArgs& a, cudaStream_t s) {
                       a.m_ld * mes, static_cast<uint64_t>(a.K) * a.m_ld * mes, 32, 32))
     return cudaErrorInvalidValue;
   auto kern = wgemm_tc_kernel<PREC, BN, TA, MB, BS>;
-  static bool configured = false;  // idempotent attribute set
-  if (!configured) {
+  static DeviceOnce configured;
+  if (configured.first()) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Sm::total);
     if (e != cudaSuccess) return e;
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
-    configured = true;
+    configured.done();
   }
   const int num_kb = (a.C + Tr::bk - 1) / Tr::bk;
   const int kbps = (num_kb + splits - 1) / splits;

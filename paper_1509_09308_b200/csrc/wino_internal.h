@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <utility>
 
 #include "../../include/wino.h"
@@ -31,6 +32,24 @@ inline int op_bytes(int prec) {
 // kernels split each landed shared-memory stage into hi = rna_tf32(x) and
 // lo = x - hi on chip, so U and V cost 4 bytes per element, not 8.
 inline int op_splits(int) { return 1; }
+
+
+// Kernel attributes (dynamic shared-memory opt-in, carveout) belong to a device
+// context, so "already configured" is tracked per (kernel call site, device):
+// a process that drives several GPUs opts every kernel in on each of them.
+// Thread-safe; concurrent first calls just set the same attributes twice.
+struct DeviceOnce {
+  std::atomic<unsigned long long> mask{0};
+  static int bit() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d & 63;
+  }
+  bool first() const { return !((mask.load(std::memory_order_acquire) >> bit()) & 1ull); }
+  void done() { mask.fetch_or(1ull << bit(), std::memory_order_release); }
+};
+// SM count of the current device (cached per device).
+int device_sms();
 
 // ---- launchers (defined in wino_transforms.cu / wino_gemm.cu) -------------
 // All return cudaError_t of the launch.

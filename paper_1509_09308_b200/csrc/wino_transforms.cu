@@ -809,11 +809,11 @@ static cudaError_t input_tma_launch(const void* d, void* V, int N, int C, int H,
   if (!encode_tmap_nchw_f32(&tmD, d, N, C, H, W, Cfg::xwb, Cfg::rows, 32))
     return cudaErrorInvalidValue;
   auto kern = input_transform_tma_kernel<M, PREC, SH>;
-  static bool configured = false;
-  if (!configured) {
+  static DeviceOnce configured;
+  if (configured.first()) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::bytes + 1024);
     max_carveout(kern);
-    configured = true;
+    configured.done();
   }
   const dim3 grid((tw + Cfg::tpx - 1) / Cfg::tpx, rows, (C + 31) / 32);
   launch_k(kern, grid, dim3(256), static_cast<size_t>(Cfg::bytes + 1024), s, tmD, V, C, pad, th,
@@ -834,11 +834,11 @@ static cudaError_t transforms_launch(const void* d, void* V, int N, int C, int H
   constexpr size_t in_smem = Cfg::bytes + 1024;
   constexpr size_t f_smem = 256 * 4 * 9 * sizeof(T) + 16;
   constexpr size_t smem = in_smem > f_smem ? in_smem : f_smem;
-  static bool configured = false;
-  if (!configured) {
+  static DeviceOnce configured;
+  if (configured.first()) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     max_carveout(kern);
-    configured = true;
+    configured.done();
   }
   const int nx = (tw + Cfg::tpx - 1) / Cfg::tpx, ncb = (C + 31) / 32;
   const long long nf = (static_cast<long long>(K) * C + 1023) / 1024;
@@ -936,11 +936,11 @@ static cudaError_t input_one(const void* d, void* V, int N, int C, int H, int W,
         (blocks >= 148 || getenv("WINO_FORCE_PLANE_INPUT") != nullptr) &&
         getenv("WINO_NO_PLANE_INPUT") == nullptr) {
       auto kp = input_transform_plane_kernel<M, PREC, CPL>;
-      static bool pconf = false;
-      if (!pconf) {
+      static DeviceOnce pconf;
+      if (pconf.first()) {
         cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
         max_carveout(kp);
-        pconf = true;
+        pconf.done();
       }
       const int n0 = row0 / th, n1 = (row0 + rows - 1) / th;
       const dim3 grid(n1 - n0 + 1, (C + CB - 1) / CB);
@@ -952,12 +952,12 @@ static cudaError_t input_one(const void* d, void* V, int N, int C, int H, int W,
   using Cfg = InCfg<M, PREC>;
   const size_t smem = sizeof(T) * Cfg::cb * Cfg::plane;
   auto kern = input_transform_kernel<M, PREC>;
-  static bool configured = false;  // benign race: idempotent attribute set
-  if (!configured) {
+  static DeviceOnce configured;
+  if (configured.first()) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
     max_carveout(kern);
-    configured = true;
+    configured.done();
   }
   const dim3 grid((tw + Cfg::tpx - 1) / Cfg::tpx, rows, (C + Cfg::cb - 1) / Cfg::cb);
   launch_k(kern, grid, dim3(256), smem, s, static_cast<const T*>(d), V, N, C, H, W, pad, th, tw,
@@ -1001,11 +1001,11 @@ static cudaError_t output_tma_launch(const void* Mbuf, void* y, int K, int th, i
                           Cfg::alpha * Cfg::alpha, es == 2))
     return cudaErrorInvalidValue;
   auto kern = output_transform_tma_kernel<M, MT>;
-  static bool configured = false;
-  if (!configured) {
+  static DeviceOnce configured;
+  if (configured.first()) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::bytes + 128);
     max_carveout(kern);
-    configured = true;
+    configured.done();
   }
   const dim3 grid(static_cast<unsigned>((Pc + kOutTP - 1) / kOutTP), (K + Cfg::OF - 1) / Cfg::OF);
   static const bool no_discard = getenv("WINO_NO_DISCARD") != nullptr;
@@ -1029,13 +1029,13 @@ cudaError_t launch_output_transform(int m, int prec, const void* Mbuf, void* y, 
     return m == 2 ? output_tma_launch<2, float>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s)
                   : output_tma_launch<4, float>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s);
   const dim3 grid(static_cast<unsigned>((Pc + 127) / 128), K);
-  static bool configured = false;
-  if (!configured) {
+  static DeviceOnce configured;
+  if (configured.first()) {
     max_carveout(output_transform_kernel<2, double>);
     max_carveout(output_transform_kernel<4, double>);
     max_carveout(output_transform_kernel<2, float>);
     max_carveout(output_transform_kernel<4, float>);
-    configured = true;
+    configured.done();
   }
   if (prec == kFP64) {
     launch_k(m == 2 ? output_transform_kernel<2, double> : output_transform_kernel<4, double>, grid,
@@ -1289,23 +1289,24 @@ static cudaError_t smallc_one(int prec, const void* d, const void* U, void* y, i
   if constexpr (smem > 227 * 1024) {  // F(4x4) fp64 with C > 4: the planner does not route here
     return cudaErrorInvalidValue;
   } else {
-    static bool configured = false;
-    static int per_sm = 1;
-    if (!configured) {
+    static DeviceOnce configured;
+    static std::atomic<int> per_sm_dev[64];  // occupancy, per device (0 = not yet known)
+    const int dbit = DeviceOnce::bit();
+    if (configured.first()) {
       max_carveout(kern);
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem));
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
-      if (per_sm < 1) per_sm = 1;
-      configured = true;
+      int occ = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
+      per_sm_dev[dbit].store(occ < 1 ? 1 : occ);
+      configured.done();
     }
+    const int per_sm = per_sm_dev[dbit].load() > 0 ? per_sm_dev[dbit].load() : 1;
     const int nkc = (K + kSmallKC - 1) / kSmallKC;
     const long long units =
         static_cast<long long>(N) * th * ((tw + kSmallTiles - 1) / kSmallTiles);
     if (units > 0x7fffffffLL) return cudaErrorInvalidValue;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = device_sms();
     long long per_kc = (static_cast<long long>(sms) * per_sm + nkc - 1) / nkc;
     if (per_kc > units) per_kc = units;
     if (per_kc < 1) per_kc = 1;

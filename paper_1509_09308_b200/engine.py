@@ -163,45 +163,93 @@ class WinogradPlan:
                                                   _stream_handle(stream)), "filter transform")
         return U
 
-    def forward(self, d, y=None, U=None, g=None, workspace=None, stream=None):
-        """y = conv(d, g) with the precomputed U (FX) or transforming g in place."""
+    def _check_host(self, x, shape, name):
+        t = _torch()
+        if not isinstance(x, t.Tensor) or x.is_cuda:
+            raise ValueError(f"{name} must be a host (CPU) tensor")
+        if tuple(x.shape) != tuple(shape) or x.dtype != self.data_dtype or not x.is_contiguous():
+            raise ValueError(f"{name}: expected contiguous {self.data_dtype} {tuple(shape)}, got "
+                             f"{x.dtype} {tuple(x.shape)}")
+        if not x.is_pinned():
+            raise ValueError(f"{name} must be in pinned host memory (asynchronous copies)")
+
+    def _operands(self, d, y, U, g, workspace, stream):
+        """Validate the device operands of one forward; allocate y / workspace when
+        absent.  Fresh allocations are made on torch's current stream, so when
+        the launch stream differs they are recorded on it (the caching allocator
+        then keeps them alive until the launch stream's work is done)."""
         t = _torch()
         c = self.cfg
         self._check_dev(d, (c.N, c.C, c.H, c.W), "d")
         if U is None and g is None:
             raise ValueError("need U or g")
-        if g is not None and U is None:
+        if U is not None:
+            if not isinstance(U, t.Tensor) or not U.is_cuda or not U.is_contiguous():
+                raise ValueError("U must be a contiguous CUDA tensor")
+            if U.numel() * U.element_size() < self.u_bytes:
+                raise ValueError(f"U: {U.numel() * U.element_size()} bytes, plan needs "
+                                 f"{self.u_bytes}")
+        else:
             self._check_dev(g, (c.K, c.C, c.R, c.S), "g")
+        fresh = []
         if y is None:
             y = t.empty(self.out_shape, dtype=self.data_dtype, device=d.device)
+            fresh.append(y)
         else:
             self._check_dev(y, self.out_shape, "y")
         if workspace is None:
             workspace = self.alloc_workspace(d.device)
+            fresh.append(workspace)
+        else:
+            if (not isinstance(workspace, t.Tensor) or not workspace.is_cuda
+                    or not workspace.is_contiguous()):
+                raise ValueError("workspace must be a contiguous CUDA tensor")
+            if workspace.numel() * workspace.element_size() < self.workspace_bytes:
+                raise ValueError(f"workspace: {workspace.numel() * workspace.element_size()} "
+                                 f"bytes, plan needs {self.workspace_bytes}")
+        if stream is not None and fresh:
+            ts = stream if isinstance(stream, t.cuda.Stream) else None
+            if ts is not None and ts != t.cuda.current_stream(d.device):
+                for x in fresh:
+                    x.record_stream(ts)
+        return y, workspace
+
+    @staticmethod
+    def _ptr(x):
+        return x.data_ptr() if x is not None else None
+
+    def forward(self, d, y=None, U=None, g=None, workspace=None, stream=None):
+        """y = conv(d, g) with the precomputed U (FX) or transforming g in place."""
+        y, workspace = self._operands(d, y, U, g, workspace, stream)
         _lib.check(_lib.lib.wino_forward(
-            self._h, d.data_ptr(), U.data_ptr() if U is not None else None,
-            g.data_ptr() if g is not None and U is None else None, y.data_ptr(),
-            workspace.data_ptr(), workspace.numel(), _stream_handle(stream)), "wino_forward")
+            self._h, d.data_ptr(), self._ptr(U), g.data_ptr() if U is None else None,
+            y.data_ptr(), workspace.data_ptr(), workspace.numel() * workspace.element_size(),
+            _stream_handle(stream)), "wino_forward")
         return y
 
     def forward_timed(self, d, y, timer: "StageTimer", U=None, g=None, workspace=None,
                       stream=None):
         """forward() plus one CUDA event per launch into `timer` (asynchronous)."""
+        y, workspace = self._operands(d, y, U, g, workspace, stream)
         _lib.check(_lib.lib.wino_forward_timed(
-            self._h, d.data_ptr(), U.data_ptr() if U is not None else None,
-            g.data_ptr() if g is not None and U is None else None, y.data_ptr(),
-            workspace.data_ptr(), workspace.numel(), _stream_handle(stream), timer._h),
-            "wino_forward_timed")
+            self._h, d.data_ptr(), self._ptr(U), g.data_ptr() if U is None else None,
+            y.data_ptr(), workspace.data_ptr(), workspace.numel() * workspace.element_size(),
+            _stream_handle(stream), timer._h), "wino_forward_timed")
         return y
 
     def forward_host(self, d_host, y_host, d_dev, y_dev, U=None, g=None, workspace=None,
                      stream=None):
-        """End-to-end call with host buffers (pinned for async copies)."""
+        """End-to-end call with host buffers (pinned, for asynchronous copies):
+        H2D of d_host into d_dev, the forward, D2H of y_dev into y_host."""
+        c = self.cfg
+        self._check_host(d_host, (c.N, c.C, c.H, c.W), "d_host")
+        self._check_host(y_host, self.out_shape, "y_host")
+        y_dev, workspace = self._operands(d_dev, y_dev, U, g, workspace, stream)
         _lib.check(_lib.lib.wino_forward_host(
-            self._h, d_host.data_ptr(), U.data_ptr() if U is not None else None,
-            g.data_ptr() if g is not None and U is None else None, y_host.data_ptr(),
-            d_dev.data_ptr(), y_dev.data_ptr(), workspace.data_ptr(), workspace.numel(),
-            _stream_handle(stream)), "wino_forward_host")
+            self._h, d_host.data_ptr(), self._ptr(U), g.data_ptr() if U is None else None,
+            y_host.data_ptr(), d_dev.data_ptr(), y_dev.data_ptr(), workspace.data_ptr(),
+            workspace.numel() * workspace.element_size(), _stream_handle(stream)),
+            "wino_forward_host")
         return y_host
 
 

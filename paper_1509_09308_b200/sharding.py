@@ -49,12 +49,21 @@ class ShardedForward:
         if self.plan is not None:
             self.U = self.plan.filter_transform(g, stream=stream)
 
-    def forward(self, d_local, y_local=None, workspace=None, stream=None):
+    def forward(self, d_local, y_local=None, workspace=None, stream=None, g=None):
+        """This rank's shard of the layer.  FX (the transformed filters from
+        set_filters) by default; pass ``g`` for the non-FX forward, which
+        transforms the replicated filters inside the call."""
         if self.plan is None:
             return None
-        if self.U is None:
-            raise ValueError("call set_filters() first")
+        if g is None and self.U is None:
+            raise ValueError("call set_filters() first (or pass g)")
+        if g is not None:
+            return self.plan.forward(d_local, y=y_local, g=g, workspace=workspace, stream=stream)
         return self.plan.forward(d_local, y=y_local, U=self.U, workspace=workspace, stream=stream)
+
+    def local_slice(self, d_global):
+        """This rank's contiguous images of a global batch tensor."""
+        return d_global[self.start:self.start + self.count]
 
 
 def gather_outputs(y_local, cfg: LayerConfig, group=None):

@@ -145,6 +145,17 @@ def test_plan_errors_map_to_reference_exceptions():
         wb.WinogradPlan(wb.LayerConfig(N=1, C=1, H=6, W=6, K=1, R=5, S=5, pad=2), 2, "fp32")
 
 
+def test_bench_algo_names_match_reference():
+    """cmd_bench accepts the reference's full BENCH_ALGOS (commands.py:26) and
+    rejects anything else with the reference's ValueError."""
+    assert wb.BENCH_ALGOS == ("direct", "direct-fp32", "f2x2", "f4x4", "f2x2-fx", "f4x4-fx",
+                              "fft")
+    with pytest.raises(ValueError, match="unknown algorithm"):
+        wb.cmd_bench(algo="f3x3")
+    with pytest.raises(ValueError, match="repeats"):
+        wb.cmd_bench(algo="direct", repeats=0)
+
+
 def test_parse_algo():
     assert wb.parse_algo("f2x2") == (2, False, None)
     assert wb.parse_algo("f4x4-fx:bf16") == (4, True, "bf16")
@@ -198,7 +209,7 @@ def test_filter_cache_key_semantics():
 def test_cli_bench_usage_errors():
     """The bench CLI maps domain errors to exit code 1 (reference cli.py:150-159)."""
     from paper_1509_09308_b200.__main__ import main
-    assert main(["bench", "--algo", "fft"]) == 1
+    assert main(["bench", "--algo", "fft2"]) == 1
     assert main(["bench", "--algo", "f4x4:int8"]) == 1
     assert main(["bench", "--batch", "0"]) == 1
 

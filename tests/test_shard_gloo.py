@@ -1,8 +1,11 @@
 """Multi-process (world_size 2, gloo, CPU) coverage of the batch-shard driver's
 host logic: each rank computes its contiguous shard of the minibatch with the
 replicated filters and no collective on the forward; the optional verification
-all_gather reassembles exactly the single-process result.  The per-rank compute
-here is the CPU oracle (test infrastructure), standing in for the GPU kernel."""
+all_gather reassembles exactly the single-process result.  The driver object
+(sharding.ShardedForward: shard bounds, per-rank plan, local slice) is the one
+bench.py --global-batch runs under torchrun; the per-rank compute here is the
+CPU oracle (test infrastructure) standing in for the GPU kernel, which needs a
+B200 (every rank's plan.forward is the C-ABI forward the GPU tests cover)."""
 import os
 import socket
 
@@ -36,7 +39,17 @@ def _worker(rank, world, port, q):
         start, count = sharding.shard_bounds(cfg.N, world, rank)
         lcfg = sharding.local_config(cfg, world, rank)
         assert lcfg.N == count
-        y_local = torch.from_numpy(O.winograd_forward(d_full[start:start + count], g, 4, cfg.pad))
+        # the batch-shard driver's host side: per-rank plan over the local shard
+        # (plan creation is host-only), its slice of the global batch
+        sf = sharding.ShardedForward(cfg, 4, "fp32", world, rank)
+        assert (sf.start, sf.count) == (start, count) and sf.cfg == lcfg
+        assert sf.plan.info["P"] == count * sf.plan.info["tiles_h"] * sf.plan.info["tiles_w"]
+        assert sf.plan.out_shape == (count, cfg.K, cfg.out_h, cfg.out_w)
+        d_local = sf.local_slice(d_full)
+        assert d_local.shape[0] == count
+        with pytest.raises(ValueError):
+            sf.forward(None)  # no filters set and no g: refused before any launch
+        y_local = torch.from_numpy(O.winograd_forward(d_local, g, 4, cfg.pad))
         y_all = sharding.gather_outputs(y_local, cfg)
         ref = O.winograd_forward(d_full, g, 4, cfg.pad)
         q.put((rank, bool(np.array_equal(y_all.numpy(), ref))))
