@@ -31,10 +31,17 @@
 
 namespace wino {
 
-// 6 warps (+8 tf32-split warps for 3xTF32)
+// warp 0 producer, warp 1 MMA, then the epilogue warps (4 for 3xTF32, whose
+// 8 split warps follow them; 8 otherwise: two per TMEM lane quarter, each
+// draining every other 32-column chunk -- the 16-bit GEMMs at large P were
+// epilogue-bound with 4: the MMA warp spent its time waiting on tempty)
 constexpr int kSplitWarps = 8;
 template <int PREC>
-constexpr int gemm_threads() { return PREC == kFP32 ? 192 + 32 * kSplitWarps : 192; }
+__host__ __device__ constexpr int gemm_epi_warps() { return PREC == kFP32 ? 4 : 8; }
+template <int PREC>
+constexpr int gemm_threads() {
+  return PREC == kFP32 ? 64 + 32 * (4 + kSplitWarps) : 64 + 32 * gemm_epi_warps<PREC>();
+}
 constexpr int kTileP = 128;        // UMMA M (tiles per CTA)
 
 template <int PREC>
@@ -134,7 +141,7 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull[b], 1);
-      ptx::mbar_init(&tempty[b], 128);
+      ptx::mbar_init(&tempty[b], 32 * gemm_epi_warps<PREC>());
     }
     for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&sfull[s], kSplitWarps);  // one per split warp
     ptx::fence_mbar_init();
@@ -237,7 +244,7 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
         ptx::umma_commit(&tfull[acc]);  // accumulator complete
       }
     }
-  } else if (warp >= 6) {
+  } else if (PREC == kFP32 && warp >= 6) {
     // ------------------------------------------------------------ 3xTF32 split
     // (warps 6.. exist only for PREC == kFP32) hi = rna_tf32(x) in place,
     // lo = x - hi into the stage's lo planes, then release the stage to MMA.
@@ -301,8 +308,13 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
     // The next 32-column TMEM load is in flight while the current one is
     // written to shared memory (two register sets, fully unrolled), and the
     // accumulator is released as soon as its last column is in registers.
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
-    float* buf0 = reinterpret_cast<float*>(smem + Sm::epi_offset + (warp - 2) * 2 * kEpiBuf);
+    constexpr int NE = gemm_epi_warps<PREC>();
+    constexpr int NH = NE / 4;   // epilogue warps per TMEM lane quarter
+    constexpr int NB = 2 / NH;   // smem staging buffers per warp (32 KB in all)
+    const int ew = warp - 2;     // epilogue warps are 2 .. 2+NE-1
+    const int q = warp & 3;      // TMEM lane quarter this warp may access
+    const int half = ew >> 2;    // this warp drains chunks ci = half, half+NH, ...
+    float* buf0 = reinterpret_cast<float*>(smem + Sm::epi_offset + ew * NB * kEpiBuf);
     const uint32_t sbuf0 = ptx::smem_u32(buf0) + 4 * lane;
     int j = 0, nbuf = 0;
     for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++j) {
@@ -316,19 +328,21 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
       constexpr int NC = BN / 32;
       uint32_t r[2][32];
-      ptx::tmem_ld_32x32b_x32(taddr, r[0]);
+      if (half < NC) ptx::tmem_ld_32x32b_x32(taddr + 32 * half, r[0]);
 #pragma unroll
-      for (int ci = 0; ci < NC; ++ci) {
+      for (int c = 0; c < (NC + NH - 1) / NH; ++c) {
+        const int ci = half + NH * c;
+        if (ci >= NC) break;
         ptx::tmem_ld_wait();  // chunk ci in registers
-        if (ci + 1 < NC) {
-          ptx::tmem_ld_32x32b_x32(taddr + 32 * (ci + 1), r[(ci + 1) & 1]);
+        if (ci + NH < NC) {
+          ptx::tmem_ld_32x32b_x32(taddr + 32 * (ci + NH), r[(c + 1) & 1]);
         } else {
           ptx::tc_fence_before();
-          ptx::mbar_arrive(&tempty[acc]);  // accumulator drained to registers
+          ptx::mbar_arrive(&tempty[acc]);  // this warp's columns drained to registers
         }
         if (dbg & 1) continue;
-        const int b = nbuf++ & 1;
-        if (lane == 0) ptx::bulk_wait_read<1>();  // the store that last used buffer b has read it
+        const int b = NB == 2 ? (nbuf++ & 1) : 0;
+        if (lane == 0) ptx::bulk_wait_read<NB - 1>();  // the store that last used buffer b has read it
         __syncwarp();
         const uint32_t sb = sbuf0 + b * kEpiBuf;
         if constexpr (MB) {  // [32 filters][32 tiles] bf16
@@ -336,13 +350,13 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
 #pragma unroll
           for (int jj = 0; jj < 32; ++jj) {
             const unsigned short h =
-                __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(r[ci & 1][jj])));
+                __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(r[c & 1][jj])));
             asm volatile("st.shared.b16 [%0], %1;" ::"r"(sh + jj * 64), "h"(h) : "memory");
           }
         } else {
 #pragma unroll
           for (int jj = 0; jj < 32; ++jj)
-            asm volatile("st.shared.b32 [%0], %1;" ::"r"(sb + jj * 128), "r"(r[ci & 1][jj]) : "memory");
+            asm volatile("st.shared.b32 [%0], %1;" ::"r"(sb + jj * 128), "r"(r[c & 1][jj]) : "memory");
         }
         ptx::fence_async_smem();
         __syncwarp();
@@ -351,8 +365,12 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
           ptx::bulk_commit();
         }
       }
+      if (half >= NC) {  // BN = 32 with two warps per quarter: nothing to drain
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&tempty[acc]);
+      }
     }
-    if (lane == 0) ptx::bulk_wait_all();
+    if (lane == 0) ptx::bulk_wait_read<0>();  // smem read; the writes drain before grid completion
   }
   ptx::tc_fence_before();
   __syncthreads();
