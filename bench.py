@@ -251,6 +251,63 @@ def run_reference_arm(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+def stage_roofline(entries, prec, fx, stream, flush, algo, batch):
+    """Live per-stage kernel timing (CUDA events on the launch stream, L2 flushed
+    before every layer) of the layer forwards in `entries` = (cfg, plan, d, y,
+    workspace, U, g, depth); the dominant stage's algorithmic bytes or flops per
+    launch over its average launch time, against the measured peak."""
+    import torch
+
+    from paper_1509_09308_b200 import engine as weng
+    stage_bytes = [0.0] * 4  # algorithmic HBM bytes
+    stage_flops = [0.0] * 4
+    timer = weng.StageTimer()
+    for (c, plan, d, y, ws, U, g, depth) in entries:
+        info = plan.info
+        a2 = info["alpha"] ** 2
+        es, ns = info["op_bytes"], info["op_splits"]
+        for _ in range(depth):
+            with torch.cuda.stream(stream):
+                flush.fill_(1)  # also gives the host a head start: no launch gaps timed
+            timer.gap()
+            plan.forward_timed(d, y, timer, U=U, g=None if fx else g, workspace=ws,
+                               stream=stream)
+            P, C, K = info["P"], c.C, c.K
+            if not fx:
+                stage_bytes[0] += 4 * 9 * K * C + ns * es * a2 * K * C
+            stage_bytes[1] += 4 * c.N * C * c.H * c.W + ns * es * a2 * C * P
+            stage_bytes[2] += ns * es * a2 * (C * P + K * C) + 4 * a2 * K * P
+            stage_bytes[3] += 4 * a2 * K * P + 4 * c.N * K * c.out_h * c.out_w
+            stage_flops[2] += 2.0 * a2 * K * C * P * (3 if prec == "fp32" else 1)
+    stage_ms, stage_n = timer.read()
+    hbm_peak, bf16_peak, peak_src = load_peaks()
+    tensor_peak = bf16_peak if prec in ("bf16", "fp16") else bf16_peak / 2  # tf32 = bf16/2
+    dom = max(range(4), key=lambda j: stage_ms[j])
+    avg_ms = stage_ms[dom] / max(stage_n[dom], 1)
+    if dom == 2:
+        achieved = stage_flops[2] / max(stage_n[2], 1) / (avg_ms / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": tensor_peak, "unit": "TFLOP/s",
+                "frac": achieved / tensor_peak, "traffic": None}
+    else:
+        achieved = stage_bytes[dom] / max(stage_n[dom], 1) / (avg_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": None}
+    traffic = load_traffic(algo, prec, batch, STAGES[dom])
+    if traffic is not None:
+        roof["traffic"] = traffic
+        roof["traffic_source"] = "ncu dram__bytes_read.sum+write.sum per launch (profiles/)"
+    roof.update({"kernel": STAGES[dom], "peak_source": f"{peak_src} (MEASURED_PEAKS.json)"
+                 if peak_src == "measured" else "fallback (B200_PROFILING.md)",
+                 "avg_launch_ms": avg_ms, "launches": stage_n[dom],
+                 "stage_share": {STAGES[j]: stage_ms[j] / max(sum(stage_ms), 1e-9)
+                                 for j in range(4)}})
+    if prec not in ("bf16", "fp16") and dom == 2:
+        roof["peak_note"] = "tf32 dense peak taken as measured bf16 / 2"
+    if prec == "fp32" and dom == 2:
+        roof["flops_note"] = "3xTF32: achieved counts all three tf32 MMA passes"
+    return roof
+
+
 # ============================================================== GPU arm
 
 def run_gpu(args) -> None:
@@ -387,53 +444,9 @@ def run_gpu(args) -> None:
     value = total_gf / t_max / 1e3  # TFLOPS, whole job
     images_per_s = images_job * args.steps / t_max
 
-    # ---- live per-stage kernel timing (CUDA events on the launch stream)
-    stage_bytes = [0.0] * 4  # algorithmic HBM bytes
-    stage_flops = [0.0] * 4
-    timer = weng.StageTimer()
-    for L in layers:
-        c, info = L["cfg"], L["plan"].info
-        a2 = info["alpha"] ** 2
-        es, ns = info["op_bytes"], info["op_splits"]
-        for _ in range(L["depth"]):
-            with torch.cuda.stream(stream):
-                flush.fill_(1)  # also gives the host a head start: no launch gaps timed
-            timer.gap()
-            L["plan"].forward_timed(L["d"], L["y"], timer, U=L["U"], g=None if fx else L["g"],
-                                    workspace=L["ws"], stream=stream)
-            P, C, K = info["P"], c.C, c.K
-            if not fx:
-                stage_bytes[0] += 4 * 9 * K * C + ns * es * a2 * K * C
-            stage_bytes[1] += 4 * c.N * C * c.H * c.W + ns * es * a2 * C * P
-            stage_bytes[2] += ns * es * a2 * (C * P + K * C) + 4 * a2 * K * P
-            stage_bytes[3] += 4 * a2 * K * P + 4 * c.N * K * c.out_h * c.out_w
-            stage_flops[2] += 2.0 * a2 * K * C * P * (3 if prec == "fp32" else 1)
-    stage_ms, stage_n = timer.read()
-    hbm_peak, bf16_peak, peak_src = load_peaks()
-    tensor_peak = bf16_peak if prec in ("bf16", "fp16") else bf16_peak / 2  # tf32 = bf16/2
-    dom = max(range(4), key=lambda j: stage_ms[j])
-    avg_ms = stage_ms[dom] / max(stage_n[dom], 1)
-    if dom == 2:
-        achieved = stage_flops[2] / max(stage_n[2], 1) / (avg_ms / 1e3) / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": tensor_peak, "unit": "TFLOP/s",
-                "frac": achieved / tensor_peak, "traffic": None}
-    else:
-        achieved = stage_bytes[dom] / max(stage_n[dom], 1) / (avg_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": None}
-    traffic = load_traffic(args.algo, prec, B, STAGES[dom])
-    if traffic is not None:
-        roof["traffic"] = traffic
-        roof["traffic_source"] = "ncu dram__bytes_read.sum+write.sum per launch (profiles/)"
-    roof.update({"kernel": STAGES[dom], "peak_source": f"{peak_src} (MEASURED_PEAKS.json)"
-                 if peak_src == "measured" else "fallback (B200_PROFILING.md)",
-                 "avg_launch_ms": avg_ms, "launches": stage_n[dom],
-                 "stage_share": {STAGES[j]: stage_ms[j] / max(sum(stage_ms), 1e-9)
-                                 for j in range(4)}})
-    if prec not in ("bf16", "fp16") and dom == 2:
-        roof["peak_note"] = "tf32 dense peak taken as measured bf16 / 2"
-    if prec == "fp32" and dom == 2:
-        roof["flops_note"] = "3xTF32: achieved counts all three tf32 MMA passes"
+    roof = stage_roofline([(L["cfg"], L["plan"], L["d"], L["y"], L["ws"], L["U"], L["g"],
+                            L["depth"]) for L in layers], prec, fx, stream, flush,
+                          args.algo, B)
 
     # ---- e2e through the C ABI with pinned host buffers (H2D + compute + D2H)
     h2d = sum(L["d_host"].numel() * 4 * L["depth"] for L in layers)
@@ -536,6 +549,129 @@ def run_gpu(args) -> None:
         dist.destroy_process_group()
 
 
+def run_chained(args) -> None:
+    """--chained: the VGG-E conv stack run as a network (network.VGGEStack):
+    each layer's output feeds the next through ReLU and 2x2 max-pool.  One step
+    = one forward of the 16-layer stack at N = --batch (per GPU); e2e copies
+    only the network input in and its output out.  Effective TFLOPS counts the
+    16 convolutions' direct-conv FLOPs (ReLU / pooling add none)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1509_09308_b200 as wb
+    from paper_1509_09308_b200.network import VGGEStack
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    m, fx, prec = wb.parse_algo(args.algo)
+    prec = args.prec or prec or "fp32"
+    if fx:
+        raise SystemExit("--chained runs the non-FX forward (filters transformed every step)")
+    B = args.batch
+    net = VGGEStack(B, m, prec, seed=0, workspace_limit=args.workspace)
+    gen = torch.Generator(device="cpu").manual_seed(1234 + rank)
+    x_host = (torch.rand(net.in_shape, generator=gen) * 2 - 1).pin_memory()
+    x = x_host.to(dev)
+    out = torch.empty(net.out_shape, device=dev)
+    out_host = torch.empty(net.out_shape).pin_memory()
+    stream = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(stream):
+        net.forward(x, out=out, stream=stream)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        net.forward(x, out=out, stream=torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    flush = torch.empty(int(args.flush_mb) << 20, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        with torch.cuda.stream(stream):
+            graph.replay()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    barrier()
+    with sampler:
+        with torch.cuda.stream(stream):
+            for a, b in evs:
+                flush.fill_(1)
+                a.record(stream)
+                graph.replay()
+                b.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    t = torch.tensor([sum(a.elapsed_time(b) for a, b in evs) / 1e3], dtype=torch.float64,
+                     device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_max = float(t.item())
+    value = net.gflop * world * args.steps / t_max / 1e3
+
+    # per-layer stage roofline on the stack's own layer inputs
+    entries = []
+    for (name, cfg, plan, g, pool) in net.layers:
+        d = torch.rand((cfg.N, cfg.C, cfg.H, cfg.W), device=dev)
+        y = torch.empty(plan.out_shape, device=dev)
+        entries.append((cfg, plan, d, y, net._ws, None, g, 1))
+    roof = stage_roofline(entries, prec, False, stream, flush, args.algo, B)
+
+    # e2e: pinned input -> device, the stack, output -> pinned host, every step
+    e2e_steps = max(1, min(args.steps, 10))
+    barrier()
+    ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        ea.record(stream)
+        for _ in range(e2e_steps):
+            x.copy_(x_host, non_blocking=True)
+            graph.replay()
+            out_host.copy_(out, non_blocking=True)
+        eb.record(stream)
+    eb.synchronize()
+    barrier()
+    te = torch.tensor([ea.elapsed_time(eb) / 1e3], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_val = net.gflop * world * e2e_steps / float(te.item()) / 1e3
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOPS",
+            "images_per_s": B * world * args.steps / t_max, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": prec, "data": "synthetic",
+            "config": {"workload": f"VGG-E conv stack chained as a network (16 conv + ReLU, "
+                                   f"2x2 max-pool per block), {args.algo} F({m}x{m},3x3), "
+                                   f"GEMM {prec}, N={B} per GPU",
+                       "algo": args.algo, "global_batch": B * world, "batch_per_gpu": B,
+                       "parallelism": f"dp{world} batch-shard (no collective)",
+                       "l2": f"flushed between timed steps ({args.flush_mb} MB write)",
+                       "cuda_graph": True, "chained": True},
+            "roofline": roof,
+            "cpu_baseline": None,
+            "e2e": {"value": e2e_val, "unit": "TFLOPS",
+                    "h2d_bytes_per_step": x_host.numel() * 4,
+                    "d2h_bytes_per_step": out_host.numel() * 4, "steps": e2e_steps,
+                    "path": "VGGEStack.forward (C ABI per layer) captured in a graph; pinned "
+                            "input copied in and output copied out every step"},
+            "gpu_launches": net.launches() * args.steps,
+            "clocks": sampler.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -553,6 +689,8 @@ def main() -> None:
                          "(default: --batch images per GPU, weak scaling)")
     ap.add_argument("--flush-mb", type=int, default=256)
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--chained", action="store_true",
+                    help="run the 16 layers as a network (ReLU + max-pool between blocks)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()
@@ -560,6 +698,8 @@ def main() -> None:
         args.warmup = 3  # timing rule: at least 3 warm-up steps
     if args.impl == "reference":
         run_reference_arm(args)
+    elif args.chained:
+        run_chained(args)
     else:
         run_gpu(args)
 

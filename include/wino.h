@@ -153,6 +153,11 @@ int wino_grad_weights(const wino_layer_t* layer, int prec, const void* d, const 
 int wino_direct_forward(const wino_layer_t* layer, int in_prec, int acc_prec, const void* d,
                         const void* g, void* y, void* stream);
 
+/* Chaining glue for the VGG-E conv stack (network.py; not on the reference's
+ * path): y = relu(x), or relu(maxpool2x2(x)) with pool != 0 (H, W even;
+ * y is (N,C,H/2,W/2)).  fp32 device pointers, enqueued on `stream`. */
+int wino_relu_pool(const float* x, float* y, int N, int C, int H, int W, int pool, void* stream);
+
 const char* wino_last_error(void);
 /* Library version string. */
 const char* wino_version(void);
