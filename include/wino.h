@@ -153,6 +153,15 @@ int wino_grad_weights(const wino_layer_t* layer, int prec, const void* d, const 
 int wino_direct_forward(const wino_layer_t* layer, int in_prec, int acc_prec, const void* d,
                         const void* g, void* y, void* stream);
 
+/* FFT overlap-and-save correlation, the reference's `fft` comparison algorithm
+ * (fftconv.py:206-275), fp64 arithmetic on hand-written kernels: tile 8 (the
+ * only size run_layer uses; others -> WINO_EUNSUPPORTED).  prec: WINO_PREC_FP32
+ * or WINO_PREC_FP64 for d / y; g is (K,C,R,S) fp64.  Device pointers. */
+int wino_fft_workspace(const wino_layer_t* layer, int tile, size_t* bytes);
+int wino_fft_forward(const wino_layer_t* layer, int prec, int tile, const void* d,
+                     const double* g, void* y, void* workspace, size_t workspace_bytes,
+                     void* stream);
+
 /* Chaining glue for the VGG-E conv stack (network.py; not on the reference's
  * path): y = relu(x), or relu(maxpool2x2(x)) with pool != 0 (H, W even;
  * y is (N,C,H/2,W/2)).  fp32 device pointers, enqueued on `stream`. */

@@ -23,7 +23,8 @@ OBJ = os.path.join(HERE, "_obj")
 OUT = os.path.join(HERE, "libwino.so")
 INCLUDE_H = os.path.normpath(os.path.join(HERE, "..", "include", "wino.h"))
 SOURCES = ("wino_api.cu", "wino_transforms.cu", "wino_gemm.cu", "wino_fused.cu",
-           "wino_fused_f2.cu", "wino_fused_f4.cu", "wino_direct.cu", "wino_net.cu")
+           "wino_fused_f2.cu", "wino_fused_f4.cu", "wino_direct.cu", "wino_net.cu",
+           "wino_fft.cu")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [*ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC"]
 

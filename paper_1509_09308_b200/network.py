@@ -56,8 +56,11 @@ class VGGEStack:
             act_max = max(act_max, N * K * H * H)
             ws_max = max(ws_max, plan.workspace_bytes)
         self.gflop = sum(gflops_direct(c) for (_, c, _, _, _) in self.layers)
+        # ping-pong activations (ReLU / pool outputs) + the conv output scratch:
+        # a layer never writes the buffer it reads
         self._a = torch.empty(act_max, dtype=torch.float32, device="cuda")
         self._b = torch.empty(act_max, dtype=torch.float32, device="cuda")
+        self._c = torch.empty(act_max, dtype=torch.float32, device="cuda")
         self._ws = torch.empty(ws_max, dtype=torch.uint8, device="cuda")
         last = self.layers[-1][1]
         self.out_shape = (N, last.K, last.H // 2, last.W // 2)
@@ -79,7 +82,7 @@ class VGGEStack:
         cur = x.contiguous()
         bufs = (self._a, self._b)
         for i, (name, cfg, plan, g, pool) in enumerate(self.layers):
-            y = bufs[i % 2][: cfg.N * cfg.K * cfg.H * cfg.W].view(cfg.N, cfg.K, cfg.H, cfg.W)
+            y = self._c[: cfg.N * cfg.K * cfg.H * cfg.W].view(cfg.N, cfg.K, cfg.H, cfg.W)
             plan.forward(cur, y=y, g=g, workspace=self._ws, stream=stream)
             oh = cfg.H // 2 if pool else cfg.H
             last = i + 1 == len(self.layers)

@@ -73,7 +73,7 @@ def test_cmd_accuracy_matches_reference(wb, gd):
 
 
 def test_fft_layer_vs_reference(wb, golden, gd):
-    """The FFT comparison algorithm (cuFFT + complex128 GEMM, the reference's
+    """The FFT comparison algorithm (hand-written fp64 DFT + complex GEMM kernels, the reference's
     tiling and fp64 transform arithmetic) against the reference's own outputs:
     fp64 within 1e-12 (relative to max|y|), fp32 within 1 fp32 rounding of the
     final cast (2^-23 relative); counters equal."""
