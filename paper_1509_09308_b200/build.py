@@ -27,6 +27,9 @@ SOURCES = ("wino_api.cu", "wino_transforms.cu", "wino_gemm.cu", "wino_fused.cu",
            "wino_fft.cu")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [*ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC"]
+# Diagnostic build: GEMM timeline stamps (tools/gemm_trace.py); part of the hash.
+if os.environ.get("WINO_BUILD_TRACE"):
+    NVCC_FLAGS.append("-DWINO_GEMM_TRACE")
 
 
 def _nvcc() -> str:

@@ -31,6 +31,35 @@
 
 namespace wino {
 
+// Diagnostic timeline (WINO_GEMM_DBG bit 64; tools/gemm_trace.py): per CTA,
+// globaltimer stamps 0 entry, 1 after griddepcontrol.wait, 2 first stage at the
+// MMA warp, 3 last commit issued, 4 first accumulator at the epilogue, 5
+// epilogue done, 6 exit, 7 first stage landed (3xTF32 split warp); slots 8-11
+// accumulate the ns the producer waited on `empty`, the MMA warp on `full` /
+// `sfull`, the MMA warp on `tempty`, and the first epilogue warp on `tfull`.
+// Compiled in only with -DWINO_GEMM_TRACE (WINO_BUILD_TRACE=1 python -m
+// paper_1509_09308_b200.build): even untaken trace branches in the MMA-issue
+// loop measurably slow it (VGG-E N=1 0.381 -> 0.389 ms).
+__device__ unsigned long long g_gemm_trace[1024][16];
+#ifdef WINO_GEMM_TRACE
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_stamp(int dbg, int slot) {
+  if ((dbg & 64) && blockIdx.x < 1024) g_gemm_trace[blockIdx.x][slot] = gtimer();
+}
+__device__ __forceinline__ void trace_add(int dbg, int slot, unsigned long long t0) {
+  if ((dbg & 64) && blockIdx.x < 1024) g_gemm_trace[blockIdx.x][slot] += gtimer() - t0;
+}
+#define TRACE_T0 ((dbg & 64) ? gtimer() : 0ull)
+#else
+__device__ __forceinline__ void trace_stamp(int, int) {}
+__device__ __forceinline__ void trace_add(int, int, unsigned long long) {}
+#define TRACE_T0 0ull
+#endif
+
 // warp 0 producer, warp 1 MMA, then the epilogue warps (4 for 3xTF32, whose
 // 8 split warps follow them; 8 otherwise: two per TMEM lane quarter, each
 // draining every other 32-column chunk -- the 16-bit GEMMs at large P were
@@ -132,6 +161,11 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
   const int lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
+    trace_stamp(dbg, 0);
+#ifdef WINO_GEMM_TRACE
+    if ((dbg & 64) && blockIdx.x < 1024)
+      for (int i = 8; i < 16; ++i) g_gemm_trace[blockIdx.x][i] = 0;
+#endif
     ptx::prefetch_tmap(&tmV);
     ptx::prefetch_tmap(&tmU);
     ptx::prefetch_tmap(&tmM);
@@ -154,6 +188,7 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
   // prologue above overlaps the predecessor (PDL); operands are read below
   griddep_launch();
   griddep_wait();
+  if (warp == 0 && lane == 0) trace_stamp(dbg, 1);
 
   auto decode = [&](int u, int& pb, int& kbk, int& comp, int& split) {
     pb = u % n_pblk;
@@ -163,19 +198,39 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
     comp = r % a2;
     split = r / a2;
   };
+  // The CTA's units are u = blockIdx.x + i * gridDim.x; step the mixed-radix
+  // (pb, kbk, comp, split) coordinates by the decoded stride instead of three
+  // integer divisions per unit (the single MMA-issuing thread and the
+  // producer are latency-bound on them at one k-block per unit, C <= 64).
+  int st_pb, st_kb, st_c, st_s;
+  decode(static_cast<int>(gridDim.x), st_pb, st_kb, st_c, st_s);
+  auto advance = [&](int& pb, int& kbk, int& comp, int& split) {
+    pb += st_pb;
+    int c = pb >= n_pblk;
+    pb -= c ? n_pblk : 0;
+    kbk += st_kb + c;
+    c = kbk >= n_kblk;
+    kbk -= c ? n_kblk : 0;
+    comp += st_c + c;
+    c = comp >= a2;
+    comp -= c ? a2 : 0;
+    split += st_s + c;
+  };
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       int it = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-        int pb, kbk, comp, split;
-        decode(u, pb, kbk, comp, split);
+      int pb, kbk, comp, split;
+      decode(blockIdx.x, pb, kbk, comp, split);
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x, advance(pb, kbk, comp, split)) {
         const int kb0 = split * kb_per_split;
         const int kb1 = min(num_kb, kb0 + kb_per_split);
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
+          const unsigned long long te0 = TRACE_T0;
           ptx::mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+          trace_add(dbg, 8, te0);
           unsigned char* st = smem + s * Sm::stage_bytes;
           // HBM holds one plane; 3xTF32's lo planes are produced on chip
           if (dbg & 2) { ptx::mbar_arrive(&full[s]); continue; }
@@ -193,56 +248,60 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = ptx::umma_idesc(Tr::fmt, kTileP, BN);
+      // descriptor of smem byte offset x = dbase + (x >> 4): the 14-bit start
+      // field cannot carry (shared window < 256 KB), so per-MMA descriptors are
+      // one 64-bit add instead of a shift / mask / or chain each
+      const uint64_t dbase = ptx::umma_desc_sw128(ptx::smem_u32(smem));
       int it = 0, j = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++j) {
-        int pb, kbk, comp, split;
-        decode(u, pb, kbk, comp, split);
+      int pb, kbk, comp, split;
+      decode(blockIdx.x, pb, kbk, comp, split);
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++j, advance(pb, kbk, comp, split)) {
         const int kb0 = split * kb_per_split;
         const int kb1 = min(num_kb, kb0 + kb_per_split);
         const int acc = j & 1;
+        const unsigned long long tt0 = TRACE_T0;
         ptx::mbar_wait(&tempty[acc], ((j >> 1) & 1) ^ 1);
+        trace_add(dbg, 10, tt0);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
+          const unsigned long long tf0 = TRACE_T0;
           if constexpr (Tr::nsplit == 2)
             ptx::mbar_wait(&sfull[s], (it / STAGES) & 1);
           else
             ptx::mbar_wait(&full[s], (it / STAGES) & 1);
+          trace_add(dbg, 9, tf0);
+          if (it == 0) trace_stamp(dbg, 2);
           ptx::tc_fence_after();
-          const uint32_t st = ptx::smem_u32(smem + s * Sm::stage_bytes);
-          const uint32_t a_hi = st, a_lo = st + Sm::a_bytes;
-          const uint32_t b_hi = st + (TA ? 1 : Tr::nsplit) * Sm::a_bytes;
-          const uint32_t b_lo = b_hi + Sm::b_bytes;
+          // stage descriptors: base + compile-time offsets (>> 4 of 16-B multiples)
+          const uint64_t dst = dbase + static_cast<uint32_t>((s * Sm::stage_bytes) >> 4);
+          constexpr uint32_t kAlo = Sm::a_bytes >> 4;
+          constexpr uint32_t kBhi = ((TA ? 1 : Tr::nsplit) * Sm::a_bytes) >> 4;
+          constexpr uint32_t kBlo = kBhi + (Sm::b_bytes >> 4);
           const uint32_t ta_hi = tmem_base + Sm::a_tmem_col + 64 * s, ta_lo = ta_hi + 32;
 #pragma unroll
           for (int k = 0; k < Tr::bk / Tr::uk; ++k) {
             if (dbg & 8) break;
-            const uint32_t off = k * 32;  // 32 bytes of K per MMA inside the swizzle atom
+            const uint32_t off = k * 2;  // 32 bytes of K per MMA inside the swizzle atom (>> 4)
             const uint32_t accum = (kb != kb0 || k != 0) ? 1u : 0u;
             if constexpr (TA) {  // A (8 tf32 columns per MMA) from tensor memory
-              ptx::umma_tf32_tmem_a(d_tmem, ta_lo + 8 * k, ptx::umma_desc_sw128(b_hi + off), idesc,
-                                    accum);
-              ptx::umma_tf32_tmem_a(d_tmem, ta_hi + 8 * k, ptx::umma_desc_sw128(b_lo + off), idesc,
-                                    1u);
-              ptx::umma_tf32_tmem_a(d_tmem, ta_hi + 8 * k, ptx::umma_desc_sw128(b_hi + off), idesc,
-                                    1u);
+              ptx::umma_tf32_tmem_a(d_tmem, ta_lo + 8 * k, dst + (kBhi + off), idesc, accum);
+              ptx::umma_tf32_tmem_a(d_tmem, ta_hi + 8 * k, dst + (kBlo + off), idesc, 1u);
+              ptx::umma_tf32_tmem_a(d_tmem, ta_hi + 8 * k, dst + (kBhi + off), idesc, 1u);
             } else if constexpr (Tr::nsplit == 2) {
-              ptx::umma<1>(d_tmem, ptx::umma_desc_sw128(a_lo + off),
-                           ptx::umma_desc_sw128(b_hi + off), idesc, accum);
-              ptx::umma<1>(d_tmem, ptx::umma_desc_sw128(a_hi + off),
-                           ptx::umma_desc_sw128(b_lo + off), idesc, 1u);
-              ptx::umma<1>(d_tmem, ptx::umma_desc_sw128(a_hi + off),
-                           ptx::umma_desc_sw128(b_hi + off), idesc, 1u);
+              ptx::umma<1>(d_tmem, dst + (kAlo + off), dst + (kBhi + off), idesc, accum);
+              ptx::umma<1>(d_tmem, dst + off, dst + (kBlo + off), idesc, 1u);
+              ptx::umma<1>(d_tmem, dst + off, dst + (kBhi + off), idesc, 1u);
             } else {
-              ptx::umma<Tr::kind>(d_tmem, ptx::umma_desc_sw128(a_hi + off),
-                                  ptx::umma_desc_sw128(b_hi + off), idesc, accum);
+              ptx::umma<Tr::kind>(d_tmem, dst + off, dst + (kBhi + off), idesc, accum);
             }
           }
           ptx::umma_commit(&empty[s]);  // frees the smem slot when these MMAs retire
         }
         ptx::umma_commit(&tfull[acc]);  // accumulator complete
       }
+      trace_stamp(dbg, 3);
     }
   } else if (PREC == kFP32 && warp >= 6) {
     // ------------------------------------------------------------ 3xTF32 split
@@ -251,14 +310,15 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
     if constexpr (Tr::nsplit == 2) {
       const int tid = threadIdx.x - 192;
       int it = 0;
-      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-        int pb, kbk, comp, split;
-        decode(u, pb, kbk, comp, split);
+      int pb, kbk, comp, split;
+      decode(blockIdx.x, pb, kbk, comp, split);
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x, advance(pb, kbk, comp, split)) {
         const int kb0 = split * kb_per_split;
         const int kb1 = min(num_kb, kb0 + kb_per_split);
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
           ptx::mbar_wait(&full[s], (it / STAGES) & 1);
+          if (it == 0 && warp == 6 && lane == 0) trace_stamp(dbg, 7);
           const uint32_t st = ptx::smem_u32(smem + s * Sm::stage_bytes);
           if constexpr (TA) {
             if (warp < 6 + 4 && !(dbg & 32)) {
@@ -317,11 +377,16 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
     float* buf0 = reinterpret_cast<float*>(smem + Sm::epi_offset + ew * NB * kEpiBuf);
     const uint32_t sbuf0 = ptx::smem_u32(buf0) + 4 * lane;
     int j = 0, nbuf = 0;
-    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++j) {
-      int pb, kbk, comp, split;
-      decode(u, pb, kbk, comp, split);
+    int pb, kbk, comp, split;
+    decode(blockIdx.x, pb, kbk, comp, split);
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++j, advance(pb, kbk, comp, split)) {
       const int acc = j & 1;
+      const unsigned long long tw0 = TRACE_T0;
       ptx::mbar_wait(&tfull[acc], (j >> 1) & 1);
+      if (ew == 0 && lane == 0) {
+        trace_add(dbg, 11, tw0);
+        if (j == 0) trace_stamp(dbg, 4);
+      }
       ptx::tc_fence_after();
       const int p0 = pb * kTileP + q * 32;
       const int z = split * a2 + comp;
@@ -371,12 +436,14 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
       }
     }
     if (lane == 0) ptx::bulk_wait_read<0>();  // smem read; the writes drain before grid completion
+    if (ew == 0 && lane == 0) trace_stamp(dbg, 5);
   }
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     __syncwarp();
     ptx::tmem_dealloc(tmem_base, Sm::tmem_cols);
+    if (lane == 0) trace_stamp(dbg, 6);
   }
 }
 
@@ -898,3 +965,11 @@ cudaError_t launch_batched_gemm(int prec, const GemmArgs& a, cudaStream_t s) {
 int gemm_kernels_per_launch(int) { return 1; }
 
 }  // namespace wino
+
+// Diagnostic only (not part of include/wino.h): copy the GEMM timeline of the
+// last launch (WINO_GEMM_DBG=64), 16 values per CTA.
+extern "C" int wino_debug_gemm_trace(unsigned long long* out, int ctas) {
+  if (ctas > 1024) ctas = 1024;
+  return cudaMemcpyFromSymbol(out, wino::g_gemm_trace, sizeof(unsigned long long) * 16 * ctas) ==
+                 cudaSuccess ? 0 : -1;
+}
