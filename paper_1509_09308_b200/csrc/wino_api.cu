@@ -433,11 +433,13 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
   if (!p->m_bf16) p->m_es = p->acc_bytes;
   // Non-FX 3xTF32 staged plans: the filter transform writes U as hi / lo planes
   // in the workspace, so the GEMM's split warps only split V (into TMEM).
-  // Worth it when U is re-read by many tile blocks; with few (the small-P deep
-  // layers at N = 1) the doubled U write sits on the critical path instead
-  // (VGG-E N=1: 0.383 -> 0.397 ms if always on; N=64: 11.6 -> 11.2 ms).
+  // Worth it when U is re-read by several tile blocks; with few (the small-P deep
+  // layers at N = 1) the doubled U write sits on the critical path instead.
+  // Threshold (WINO_USPLIT_MIN_PBLK) measured on VGG-E F2 fp32 N=1: 16 -> 0.3755,
+  // 4 -> 0.3705, 1 -> 0.385 ms; N=64: 11.6 -> 11.2 ms with it.
+  static const int usplit_min = getenv("WINO_USPLIT_MIN_PBLK") ? atoi(getenv("WINO_USPLIT_MIN_PBLK")) : 4;
   p->u_split2 = (prec == kFP32 && p->path == kPathStaged && !p->smallc &&
-                 gemm_tmem_a_enabled() && (p->P + 127) / 128 >= 16 &&
+                 gemm_tmem_a_enabled() && (p->P + 127) / 128 >= usplit_min &&
                  getenv("WINO_NO_USPLIT") == nullptr) ? 1 : 0;
   p->u_ws = p->u_split2 ? 2 * p->u_bytes : p->u_bytes;
   auto set_m_bytes = [&] {

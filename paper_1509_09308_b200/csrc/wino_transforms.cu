@@ -1025,7 +1025,14 @@ cudaError_t launch_output_transform(int m, int prec, const void* Mbuf, void* y, 
     return m == 2 ? output_tma_launch<2, __nv_bfloat16>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s)
                   : output_tma_launch<4, __nv_bfloat16>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s);
   }
-  if (prec != kFP64 && splits == 1 && getenv("WINO_NO_TMA_OUTPUT") == nullptr)
+  // F(4x4) chunks of <= 256 tiles (conv3-5 at N = 1) take the per-thread
+  // kernel: VGG-E F4 fp16 N=1 0.294 -> 0.275 ms.  For F(2x2) the TMA box stays
+  // faster on every chunk size in the pass (F2 fp32 N=1: 0.371 vs 0.377 ms).
+  // WINO_OUT_TMA_MIN overrides the F(4x4) tile threshold.
+  static const long long tma_min =
+      getenv("WINO_OUT_TMA_MIN") ? atoll(getenv("WINO_OUT_TMA_MIN")) : 256;
+  if (prec != kFP64 && splits == 1 && (m == 2 || Pc > tma_min) &&
+      getenv("WINO_NO_TMA_OUTPUT") == nullptr)
     return m == 2 ? output_tma_launch<2, float>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s)
                   : output_tma_launch<4, float>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s);
   const dim3 grid(static_cast<unsigned>((Pc + 127) / 128), K);
