@@ -35,6 +35,8 @@ struct wino_plan_s {
   int m_es;                          // M element bytes
   size_t u_bytes, v_bytes, m_bytes;  // v/m per full chunk
   int u_split2;                      // non-FX 3xTF32 staged: U as hi/lo planes in the workspace
+  int gemm_tr;                       // 3xTF32 small P: filters on the MMA M side (bn = tiles)
+  int v_split2;                      // with gemm_tr: V written as tf32 hi / lo planes
   size_t u_ws;                       // workspace bytes of a forward-computed U
   size_t staging_bytes;              // V + M of the chunks in flight (+ fused partials)
 };
@@ -290,6 +292,21 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
   // (F(4x4) fp64 with C > 4 would exceed the small-C kernel's shared memory)
   p->smallc = L.C <= ((prec == kFP64 && m == 4) ? 4 : kSmallCMax);
 
+  // 3xTF32 with more filters than tiles (K > P: the deep layers at N = 1):
+  // filters on the MMA's 128-row side (A, split into TMEM) and the tiles on N
+  // (bn = 32 / 64 / 128 tiles), with V pre-split into tf32 hi / lo planes by
+  // the input transform (off the critical path there: the filter transform is
+  // longer), so no operand is split in shared memory.  WINO_NO_GEMM_TR=1
+  // disables; WINO_GEMM_TR_MAXP bounds P (default 256).
+  p->gemm_tr = 0;
+  static const long long tr_maxp =
+      getenv("WINO_GEMM_TR_MAXP") ? atoll(getenv("WINO_GEMM_TR_MAXP")) : 256;
+  if (prec == kFP32 && gemm_tmem_a_enabled() && !p->smallc && p->P <= tr_maxp &&
+      static_cast<long long>(L.K) > p->P && L.K >= 128 && getenv("WINO_NO_GEMM_TR") == nullptr) {
+    p->gemm_tr = 1;
+    p->bn = p->P <= 32 ? 32 : p->P <= 64 ? 64 : 128;
+  }
+
   // ---- chunk planner: whole tile rows, V + M staging within the budget
   const size_t budget = workspace_limit ? workspace_limit : kDefaultWorkspace;
   // bf16 GEMM: M is staged in bf16.  The accumulation stays fp32 (TMEM); the one
@@ -315,7 +332,9 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
   if (prec != kFP64 && p->num_chunks == 1) {
     const int sms = gemm_device_sms();
     const int num_kb = gemm_num_kblocks(prec, L.C);
-    const long long units = ((p->chunk_tiles + 127) / 128) * ((L.K + p->bn - 1) / p->bn) * p->a2;
+    const long long units =
+        p->gemm_tr ? ((L.K + 127) / 128) * ((p->chunk_tiles + p->bn - 1) / p->bn) * p->a2
+                   : ((p->chunk_tiles + 127) / 128) * ((L.K + p->bn - 1) / p->bn) * p->a2;
     if (units < sms && num_kb > 1) {
       // waves x k-steps per unit (+2 for the unit's fill and epilogue) + half a
       // k-step per M slice the output transform sums; ties -> fewer splits
@@ -339,9 +358,12 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
       }
     }
   }
+  // gemm_tr plans take V from the input transform as tf32 hi / lo planes, so
+  // the GEMM's B operand needs no on-chip split (WINO_NO_VSPLIT=1 disables)
+  p->v_split2 = (p->gemm_tr && getenv("WINO_NO_VSPLIT") == nullptr) ? 1 : 0;
   p->v_bytes = p->smallc ? 0
-                        : align_up(static_cast<size_t>(p->nsplit) * p->a2 * p->chunk_tiles *
-                                       p->c_pad * p->esize,
+                        : align_up(static_cast<size_t>(p->nsplit) * (p->v_split2 ? 2 : 1) *
+                                       p->a2 * p->chunk_tiles * p->c_pad * p->esize,
                                    1024);
   if (p->smallc) {  // no transform-space staging at all
     p->num_chunks = 1;
@@ -369,6 +391,7 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
   }
   p->fsplits = 1;
   p->ypart_bytes = 0;
+  if (p->path != kPathStaged) p->gemm_tr = p->v_split2 = 0;
   if (p->path != kPathStaged) {
     if (p->path == kPathFused) {
       p->num_chunks = 1;
@@ -422,8 +445,8 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
     p->rows_per_chunk = static_cast<int>(r2);
     p->num_chunks = (p->rows_total + p->rows_per_chunk - 1) / p->rows_per_chunk;
     p->chunk_tiles = static_cast<long long>(p->rows_per_chunk) * p->tw;
-    p->v_bytes = align_up(static_cast<size_t>(p->nsplit) * p->a2 * p->chunk_tiles * p->c_pad *
-                              p->esize,
+    p->v_bytes = align_up(static_cast<size_t>(p->nsplit) * (p->v_split2 ? 2 : 1) * p->a2 *
+                              p->chunk_tiles * p->c_pad * p->esize,
                           1024);
     p->m_ld = static_cast<long long>(align_up(static_cast<size_t>(p->chunk_tiles), 64));
     p->overlap = p->num_chunks > 1;
@@ -438,7 +461,7 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
   // Threshold (WINO_USPLIT_MIN_PBLK) measured on VGG-E F2 fp32 N=1: 16 -> 0.3755,
   // 4 -> 0.3705, 1 -> 0.385 ms; N=64: 11.6 -> 11.2 ms with it.
   static const int usplit_min = getenv("WINO_USPLIT_MIN_PBLK") ? atoi(getenv("WINO_USPLIT_MIN_PBLK")) : 4;
-  p->u_split2 = (prec == kFP32 && p->path == kPathStaged && !p->smallc &&
+  p->u_split2 = (prec == kFP32 && p->path == kPathStaged && !p->smallc && !p->gemm_tr &&
                  gemm_tmem_a_enabled() && (p->P + 127) / 128 >= usplit_min &&
                  getenv("WINO_NO_USPLIT") == nullptr) ? 1 : 0;
   p->u_ws = p->u_split2 ? 2 * p->u_bytes : p->u_bytes;
@@ -664,7 +687,7 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
                          !chunk_overlap && static_cast<long long>(p->L.K) > p->P;
     if (in_side) {
       input_enqueued = true;
-      cudaError_t e = launch_input_transform(p->m, p->prec, d, ws + p->u_ws, p->L.N, p->L.C,
+      cudaError_t e = launch_input_transform(p->m, p->v_split2 ? kFP32S : p->prec, d, ws + p->u_ws, p->L.N, p->L.C,
                                              p->L.H, p->L.W, p->L.pad, p->th, p->tw, 0,
                                              p->rows_total, p->P, p->c_pad, side->st);
       if (e != cudaSuccess) return cuda_fail(e, "input transform");
@@ -760,13 +783,13 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
     unsigned char* Mb = V + p->v_bytes;
     cudaError_t e = cudaSuccess;
     if (!(input_enqueued && ch == 0)) {
-      e = launch_input_transform(p->m, p->prec, d, V, L.N, L.C, L.H, L.W, L.pad, p->th, p->tw,
+      e = launch_input_transform(p->m, p->v_split2 ? kFP32S : p->prec, d, V, L.N, L.C, L.H, L.W, L.pad, p->th, p->tw,
                                  row0, rows, Pc, p->c_pad, cs);
       if (e != cudaSuccess) return cuda_fail(e, "input transform");
     }
     tm.mark(1);
     GemmArgs ga{V, U, Mb, p->a2, L.K, L.C, p->c_pad, Pc, p->bn, p->splits, p->m_ld, p->m_bf16,
-                u_split ? 1 : 0};
+                (u_split || p->v_split2) ? 1 : 0, p->gemm_tr};
     if (!side_chunk) {
       e = join_filters();
       if (e != cudaSuccess) return cuda_fail(e, "filter transform join");

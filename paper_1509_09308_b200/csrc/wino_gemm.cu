@@ -135,7 +135,12 @@ __device__ __forceinline__ void split_region(uint32_t hi, int n, int lo_off, int
 // MB: store M as bf16 (the bf16 GEMM's staged M, wino_api.cu planner).
 // BS (with TA): U arrives as hi / lo planes (filter transform split2), so the
 // B operand needs no on-chip split; TMA loads both planes into the stage.
-template <int PREC, int BN, bool TA, bool MB, bool BS = false>
+// TRN (3xTF32, K > P layers): roles swapped -- A (M side, split into TMEM) is
+// the filter block U[comp][128 filters][c], B (N side) a BN-tile block of V, so
+// a 49-tile layer runs 128 x 64 MMAs instead of 128 x 128 with 79 empty rows;
+// the epilogue writes the transposed TMEM tile into the same M[z][k][p] layout
+// through a 128B-swizzled staging box.
+template <int PREC, int BN, bool TA, bool MB, bool BS = false, bool TRN = false>
 __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
     wgemm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmU,
                     const __grid_constant__ CUtensorMap tmM, int a2, int num_kb,
@@ -410,7 +415,15 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
         if (lane == 0) ptx::bulk_wait_read<NB - 1>();  // the store that last used buffer b has read it
         __syncwarp();
         const uint32_t sb = sbuf0 + b * kEpiBuf;
-        if constexpr (MB) {  // [32 filters][32 tiles] bf16
+        if constexpr (TRN) {  // thread = filter row, r[jj] = tile jj: swizzled 128-B rows
+          const uint32_t rowb = sb - 4 * lane + 128 * lane;  // sbuf0 carries 4*lane
+#pragma unroll
+          for (int c4 = 0; c4 < 8; ++c4)
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowb + ((c4 ^ (lane & 7)) << 4)),
+                         "r"(r[c & 1][4 * c4]), "r"(r[c & 1][4 * c4 + 1]), "r"(r[c & 1][4 * c4 + 2]),
+                         "r"(r[c & 1][4 * c4 + 3])
+                         : "memory");
+        } else if constexpr (MB) {  // [32 filters][32 tiles] bf16
           const uint32_t sh = sb - 2 * lane;  // sbuf0 carries 4*lane
 #pragma unroll
           for (int jj = 0; jj < 32; ++jj) {
@@ -426,7 +439,10 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
         ptx::fence_async_smem();
         __syncwarp();
         if (lane == 0) {
-          ptx::tma_store_3d(&tmM, buf0 + b * (kEpiBuf / 4), p0, kbk * BN + 32 * ci, z);
+          if constexpr (TRN)  // (tile, filter) = (column block, TMEM lane block)
+            ptx::tma_store_3d(&tmM, buf0 + b * (kEpiBuf / 4), kbk * BN + 32 * ci, p0, z);
+          else
+            ptx::tma_store_3d(&tmM, buf0 + b * (kEpiBuf / 4), p0, kbk * BN + 32 * ci, z);
           ptx::bulk_commit();
         }
       }
@@ -845,27 +861,34 @@ static int gemm_dbg() {  // diagnostic: 1 = skip M stores, 2 = skip operand load
   return v;
 }
 
-template <int PREC, int BN, bool TA, bool MB = false, bool BS = false>
+template <int PREC, int BN, bool TA, bool MB = false, bool BS = false, bool TRN = false>
 static cudaError_t launch_tc(const GemmArgs& a, cudaStream_t s) {
   using Tr = GemmTraits<PREC>;
   using Sm = GemmSmem<PREC, BN, TA>;
-  alignas(64) CUtensorMap tmV, tmU;
+  static_assert(!TRN || (TA && !MB), "TRN: 3xTF32 TMEM-A, fp32 M");
+  alignas(64) CUtensorMap tmV, tmU;  // the A (128-row) and B (BN-row) operand maps
   const uint64_t es = Tr::esize;
   const uint64_t planes = static_cast<uint64_t>(op_splits(PREC)) * a.a2;  // planes in HBM
   const uint64_t u_planes = BS ? 2 * planes : planes;
-  if (!encode_tmap_3d(&tmV, PREC, a.V, a.C, a.Pc, planes, a.c_pad * es, a.Pc * a.c_pad * es,
+  const void* A = TRN ? a.U : a.V;
+  const void* B = TRN ? a.V : a.U;
+  const uint64_t a_rows = TRN ? static_cast<uint64_t>(a.K) : static_cast<uint64_t>(a.Pc);
+  const uint64_t b_rows = TRN ? static_cast<uint64_t>(a.Pc) : static_cast<uint64_t>(a.K);
+  if (!encode_tmap_3d(&tmV, PREC, A, a.C, a_rows, planes, a.c_pad * es, a_rows * a.c_pad * es,
                       Tr::bk, kTileP))
     return cudaErrorInvalidValue;
-  if (!encode_tmap_3d(&tmU, PREC, a.U, a.C, a.K, u_planes, a.c_pad * es,
-                      static_cast<uint64_t>(a.K) * a.c_pad * es, Tr::bk, BN))
+  if (!encode_tmap_3d(&tmU, PREC, B, a.C, b_rows, u_planes, a.c_pad * es,
+                      b_rows * a.c_pad * es, Tr::bk, BN))
     return cudaErrorInvalidValue;
   const int splits = a.splits < 1 ? 1 : a.splits;
   alignas(64) CUtensorMap tmM;
   constexpr uint64_t mes = MB ? 2 : 4;  // M element bytes
-  if (!encode_tmap_3d(&tmM, MB ? -2 : -1, a.M, a.Pc, a.K, static_cast<uint64_t>(splits) * a.a2,
-                      a.m_ld * mes, static_cast<uint64_t>(a.K) * a.m_ld * mes, 32, 32))
+  // TRN stages 128B-swizzled [32 filters][32 tiles] boxes (conflict-free row stores)
+  if (!encode_tmap_3d(&tmM, TRN ? kFP32 : (MB ? -2 : -1), a.M, a.Pc, a.K,
+                      static_cast<uint64_t>(splits) * a.a2, a.m_ld * mes,
+                      static_cast<uint64_t>(a.K) * a.m_ld * mes, 32, 32))
     return cudaErrorInvalidValue;
-  auto kern = wgemm_tc_kernel<PREC, BN, TA, MB, BS>;
+  auto kern = wgemm_tc_kernel<PREC, BN, TA, MB, BS, TRN>;
   static DeviceOnce configured;
   if (configured.first()) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -877,8 +900,9 @@ static cudaError_t launch_tc(const GemmArgs& a, cudaStream_t s) {
   }
   const int num_kb = (a.C + Tr::bk - 1) / Tr::bk;
   const int kbps = (num_kb + splits - 1) / splits;
-  const int n_pblk = static_cast<int>((a.Pc + kTileP - 1) / kTileP);
-  const int n_kblk = (a.K + BN - 1) / BN;
+  // A-side (128-row) and B-side (BN-row) block counts
+  const int n_pblk = static_cast<int>((a_rows + kTileP - 1) / kTileP);
+  const int n_kblk = static_cast<int>((b_rows + BN - 1) / BN);
   const long long units = static_cast<long long>(n_pblk) * n_kblk * a.a2 * splits;
   if (units > 0x7fffffffLL) return cudaErrorInvalidValue;
   const int grid = static_cast<int>(units < num_sms() ? units : num_sms());
@@ -901,10 +925,21 @@ static cudaError_t launch_prec(const GemmArgs& a, cudaStream_t s) {
   if constexpr (PREC == kFP32) {  // 3xTF32: A operand through tensor memory (BN <= 128)
     static const bool tmem_a = getenv("WINO_NO_TMEM_A") == nullptr;
     static const bool pair = getenv("WINO_GEMM_2SM") != nullptr;
-    if (tmem_a && pair && (a.bn == 64 || a.bn == 128)) {
+    if (tmem_a && pair && !a.tr && (a.bn == 64 || a.bn == 128)) {
       if (a.b_split)
         return a.bn == 64 ? launch_tc2<64, true>(a, s) : launch_tc2<128, true>(a, s);
       return a.bn == 64 ? launch_tc2<64, false>(a, s) : launch_tc2<128, false>(a, s);
+    }
+    if (tmem_a && a.tr) {  // b_split: V arrives as hi / lo planes (input transform)
+      switch (a.bn * 2 + (a.b_split ? 1 : 0)) {
+        case 64: return launch_tc<PREC, 32, true, false, false, true>(a, s);
+        case 65: return launch_tc<PREC, 32, true, false, true, true>(a, s);
+        case 128: return launch_tc<PREC, 64, true, false, false, true>(a, s);
+        case 129: return launch_tc<PREC, 64, true, false, true, true>(a, s);
+        case 256: return launch_tc<PREC, 128, true, false, false, true>(a, s);
+        case 257: return launch_tc<PREC, 128, true, false, true, true>(a, s);
+        default: return cudaErrorInvalidValue;
+      }
     }
     if (tmem_a && a.b_split) {
       switch (a.bn) {

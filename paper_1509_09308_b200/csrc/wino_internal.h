@@ -18,6 +18,9 @@ enum Prec : int {
   kBF16 = WINO_PREC_BF16,
   kFP16 = WINO_PREC_FP16,
   kFP64 = WINO_PREC_FP64,  // fp64 data end to end (CUDA-core GEMM)
+  // internal, input transform only: fp32 V written as tf32 hi / lo planes (the
+  // 3xTF32 GEMM's B operand pre-split, WINO_PREC_FP32 plans with filters on M)
+  kFP32S = 16,
 };
 
 inline int op_bytes(int prec) {
@@ -116,6 +119,7 @@ struct GemmArgs {
   long long m_ld;  // M row stride (>= Pc, multiple of 4 -- 8 for bf16 M -- for the TMA store)
   int m_bf16 = 0;  // bf16 GEMM only: M staged as bf16 (see wino_api.cu planner)
   int b_split = 0; // 3xTF32 only: U holds [hi planes][lo planes] (no on-chip B split)
+  int tr = 0;      // 3xTF32 TMEM-A only: filters on the MMA M side, bn = tiles per unit
 };
 int gemm_num_kblocks(int prec, int C);
 int gemm_device_sms();

@@ -27,6 +27,16 @@ struct OpStore<kFP32> {  // 3xTF32: plain fp32 in memory; the GEMM splits hi/lo 
   }
 };
 template <>
+struct OpStore<kFP32S> {  // 3xTF32 pre-split: hi = rna_tf32(x) at idx, lo = x - hi one plane on
+  using T = float;
+  __device__ static void put(void* base, size_t idx, size_t plane, float x) {
+    uint32_t h;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+    static_cast<float*>(base)[idx] = __uint_as_float(h);
+    static_cast<float*>(base)[idx + plane] = x - __uint_as_float(h);
+  }
+};
+template <>
 struct OpStore<kTF32> {
   using T = float;
   __device__ static void put(void* base, size_t idx, size_t, float x) {
@@ -971,6 +981,7 @@ static cudaError_t input_dispatch(int prec, const void* d, void* V, int N, int C
                                   int c_pad, cudaStream_t s) {
   switch (prec) {
     case kFP32: return input_one<M, kFP32>(d, V, N, C, H, W, pad, th, tw, row0, rows, Pc, c_pad, s);
+    case kFP32S: return input_one<M, kFP32S>(d, V, N, C, H, W, pad, th, tw, row0, rows, Pc, c_pad, s);
     case kTF32: return input_one<M, kTF32>(d, V, N, C, H, W, pad, th, tw, row0, rows, Pc, c_pad, s);
     case kBF16: return input_one<M, kBF16>(d, V, N, C, H, W, pad, th, tw, row0, rows, Pc, c_pad, s);
     case kFP16: return input_one<M, kFP16>(d, V, N, C, H, W, pad, th, tw, row0, rows, Pc, c_pad, s);
