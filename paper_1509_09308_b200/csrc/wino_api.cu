@@ -498,7 +498,9 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
 // Non-FX forwards of this plan launch the filter and input transforms as one
 // kernel (staged, single chunk, 16-bit operands, TMA-eligible input).
 static bool plan_combines_transforms(const wino_plan_s* p) {
-  return p->path == kPathStaged && !p->smallc && (p->prec == kBF16 || p->prec == kFP16) &&
+  static const bool fp32 = getenv("WINO_FP32_COMBINED") != nullptr;
+  return p->path == kPathStaged && !p->smallc &&
+         (p->prec == kBF16 || p->prec == kFP16 || (fp32 && p->prec == kFP32)) &&
          p->num_chunks == 1 && transforms_combinable(p->prec, p->L.W, p->L.pad);
 }
 
@@ -675,7 +677,7 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
   const bool u_split = !U && p->u_split2;  // U computed here as hi / lo planes
   if (combined) {
     const wino_layer_t& Lc = p->L;
-    cudaError_t e = launch_transforms(p->m, p->prec, d, ws + p->u_ws, Lc.N, Lc.C, Lc.H, Lc.W,
+    cudaError_t e = launch_transforms(p->m, p->v_split2 ? kFP32S : p->prec, d, ws + p->u_ws, Lc.N, Lc.C, Lc.H, Lc.W,
                                       Lc.pad, p->th, p->tw, p->rows_total, p->P, p->c_pad, g, ws,
                                       Lc.K, u_split, s);
     if (e != cudaSuccess) return cuda_fail(e, "filter + input transforms");

@@ -806,7 +806,8 @@ __global__ void __launch_bounds__(256) transforms_kernel(
     griddep_wait();
     T* sg = reinterpret_cast<T*>((reinterpret_cast<uintptr_t>(smem_raw) + 15) &
                                  ~static_cast<uintptr_t>(15));
-    filter_block<M, PREC, 4, SPLIT2>(g, U, K, C, c_pad, b - n_in, sg);
+    // (kFP32S splits V only: U stays one fp32 plane, the A operand split on chip)
+    filter_block<M, PREC == kFP32S ? kFP32 : PREC, 4, SPLIT2>(g, U, K, C, c_pad, b - n_in, sg);
   }
 }
 
@@ -900,6 +901,7 @@ cudaError_t launch_transforms(int m, int prec, const void* d, void* V, int N, in
   if (m == 2) {
     switch (prec) {
       case kFP32: WINO_TP(2, kFP32);
+      case kFP32S: WINO_TP(2, kFP32S);
       case kTF32: WINO_TP(2, kTF32);
       case kBF16: WINO_TP(2, kBF16);
       case kFP16: WINO_TP(2, kFP16);
@@ -908,6 +910,7 @@ cudaError_t launch_transforms(int m, int prec, const void* d, void* V, int N, in
   }
   switch (prec) {
     case kFP32: WINO_TP(4, kFP32);
+    case kFP32S: WINO_TP(4, kFP32S);
     case kTF32: WINO_TP(4, kTF32);
     case kBF16: WINO_TP(4, kBF16);
     case kFP16: WINO_TP(4, kFP16);

@@ -419,3 +419,36 @@ def test_padding_variants(wb, pad):
             assert O.max_abs_error(y, ref) < (5e-4 if m == 2 else 5e-3), (pad, H, W, m)
             yb = _run(wb, d, g, pad, m, prec="bf16")
             assert O.max_abs_error(yb, ref) / np.abs(ref).max() <= REL_TOL[("bf16", m)]
+
+
+@pytest.mark.parametrize("m", [2, 4])
+@pytest.mark.parametrize("N,C,H,K", [
+    (1, 40, 10, 136),   # P = 25 (F2) / 9 (F4): bn = 32 tiles, ragged K
+    (1, 96, 15, 300),   # P = 64 / 16: bn = 64 / 32, K not a multiple of 128
+    (2, 64, 19, 520),   # P = 200 / 50: bn = 128 (two tile blocks) / 64, ragged H
+    (1, 512, 14, 512),  # conv5: split-C with the transposed GEMM
+])
+@pytest.mark.parametrize("vsplit", [True, False])
+def test_transposed_gemm_k_gt_p(wb, monkeypatch, m, N, C, H, K, vsplit):
+    """3xTF32 layers with more filters than tiles run the GEMM with the filters on
+    the MMA's M side (TRN variant) and, by default, V pre-split into tf32 hi/lo
+    planes by the input transform; both must meet the fp32 gates and match the
+    default-orientation GEMM to the last bits of the accumulation order."""
+    import torch
+    if not vsplit:
+        monkeypatch.setenv("WINO_NO_VSPLIT", "1")
+    cfg = wb.LayerConfig(N=N, C=C, H=H, W=H, K=K, pad=1)
+    plan = wb.WinogradPlan(cfg, m, "fp32")
+    th = (H + m - 1) // m
+    assert plan.info["P"] == N * th * th < K
+    d = O.fill_uniform((N, C, H, H), 41)
+    g = O.fill_uniform((K, C, 3, 3), 42)
+    dd, gg = torch.from_numpy(d).cuda(), torch.from_numpy(g).cuda()
+    y = plan.forward(dd, g=gg).cpu().numpy()
+    ref = O.direct_forward(d, g, 1)
+    assert O.max_abs_error(y, ref) < (5e-4 if m == 2 else 5e-3)
+    yo = O.winograd_forward(d, g, m, 1)
+    assert np.abs(y - yo).max() <= 2e-5 * (1 + np.abs(yo).max())
+    monkeypatch.setenv("WINO_NO_GEMM_TR", "1")
+    y2 = wb.WinogradPlan(cfg, m, "fp32").forward(dd, g=gg).cpu().numpy()
+    assert np.abs(y - y2).max() <= 4e-6 * (1 + np.abs(y2).max())
