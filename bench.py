@@ -350,21 +350,35 @@ def run_gpu(args) -> None:
         else:
             cfg = wb.LayerConfig(N=B, C=C, H=H, W=H, K=K, pad=1)
             plan = weng.WinogradPlan(cfg, m, prec, workspace_limit=args.workspace)
-        # synthetic U[-1,1) data (this rank's shard) and replicated filters
-        d_host = (torch.rand((B, C, H, H), generator=gen) * 2 - 1).pin_memory()
-        g_host = torch.rand((K, C, 3, 3), generator=torch.Generator().manual_seed(i)) * 2 - 1
-        d = d_host.to(dev)
-        g = g_host.to(dev)
-        y = torch.empty(plan.out_shape, dtype=torch.float32, device=dev)
-        y_host = torch.empty(plan.out_shape, dtype=torch.float32).pin_memory()
+        # synthetic U[-1,1) data (this rank's shard) and replicated filters.  Every
+        # instance of a repeated layer (conv3.2 x3, conv4.2 x3, conv5 x4) has its own
+        # input and filters, as in the network (the reference's cmd_bench re-runs
+        # one input; --reuse-depth-inputs restores that, which reads the repeats'
+        # filters from warm L2)
+        ninst = 1 if args.reuse_depth_inputs else depth
+        inst = []
+        for j in range(ninst):
+            d_host = (torch.rand((B, C, H, H), generator=gen) * 2 - 1).pin_memory()
+            g_host = torch.rand((K, C, 3, 3),
+                                generator=torch.Generator().manual_seed(100 * i + j)) * 2 - 1
+            d = d_host.to(dev)
+            g = g_host.to(dev)
+            y = torch.empty(plan.out_shape, dtype=torch.float32, device=dev)
+            y_host = torch.empty(plan.out_shape, dtype=torch.float32).pin_memory()
+            if strong and fx:
+                sh = sharding.ShardedForward(gcfg, m, prec, world, rank,
+                                             workspace_limit=args.workspace)
+                sh.set_filters(g)
+                inst.append(dict(d=d, g=g, y=y, U=sh.U, shard=sh, d_host=d_host, y_host=y_host))
+            else:
+                inst.append(dict(d=d, g=g, y=y, U=plan.filter_transform(g) if fx else None,
+                                 shard=shard if strong else None, d_host=d_host, y_host=y_host))
         ws = plan.alloc_workspace(dev)
-        U = plan.filter_transform(g) if fx else None
-        if strong and fx:
-            shard.set_filters(g)
-            U = shard.U
-        layers.append(dict(lbl=lbl, C=C, H=H, K=K, depth=depth, cfg=cfg, plan=plan, d=d, g=g,
-                           shard=shard if strong else None,
-                           y=y, ws=ws, U=U, d_host=d_host, y_host=y_host,
+        calls = [inst[j % ninst] for j in range(depth)]
+        layers.append(dict(lbl=lbl, C=C, H=H, K=K, depth=depth, cfg=cfg, plan=plan,
+                           d=inst[0]["d"], g=inst[0]["g"], y=inst[0]["y"], U=inst[0]["U"],
+                           shard=shard if strong else None, ws=ws, calls=calls,
+                           d_host=inst[0]["d_host"], y_host=inst[0]["y_host"],
                            gf=gflop_direct(B, C, H, K)))
     gf_step = sum(L["gf"] * L["depth"] for L in layers)  # this rank's share
     # whole-job GFLOP per step: every rank's shard (weak: world x B images;
@@ -380,12 +394,12 @@ def run_gpu(args) -> None:
 
     def step_body(s):
         for L in layers:
-            for _ in range(L["depth"]):
-                if L["shard"] is not None:  # batch-shard driver (strong scaling)
-                    L["shard"].forward(L["d"], y_local=L["y"], workspace=L["ws"], stream=s,
-                                       g=None if fx else L["g"])
+            for c in L["calls"]:
+                if c["shard"] is not None:  # batch-shard driver (strong scaling)
+                    c["shard"].forward(c["d"], y_local=c["y"], workspace=L["ws"], stream=s,
+                                       g=None if fx else c["g"])
                 else:
-                    L["plan"].forward(L["d"], y=L["y"], U=L["U"], g=None if fx else L["g"],
+                    L["plan"].forward(c["d"], y=c["y"], U=c["U"], g=None if fx else c["g"],
                                       workspace=L["ws"], stream=s)
 
     # capture the whole step in one CUDA graph (launch-bound at N=1)
@@ -475,12 +489,12 @@ def run_gpu(args) -> None:
     def e2e_step():
         call = 0
         for li, L in enumerate(layers):
-            for _ in range(L["depth"]):
+            for c in L["calls"]:
                 si = call % E2E_STREAMS
                 call += 1
                 d_dev, y_dev, ws, y_host = e2e_bufs[si][li]
-                L["plan"].forward_host(L["d_host"], y_host, d_dev, y_dev, U=L["U"],
-                                       g=None if fx else L["g"], workspace=ws,
+                L["plan"].forward_host(c["d_host"], y_host, d_dev, y_dev, U=c["U"],
+                                       g=None if fx else c["g"], workspace=ws,
                                        stream=e2e_streams[si])
 
     def e2e_fork(ev):
@@ -534,6 +548,9 @@ def run_gpu(args) -> None:
                                       + (", sharding.ShardedForward" if strong else ""),
                        "workspace_limit": args.workspace,
                        "l2": f"flushed between timed steps ({args.flush_mb} MB write)",
+                       "layer_instances": ("one input/filter set per shape, re-run depth times"
+                                           if args.reuse_depth_inputs else
+                                           "distinct input and filters for each of the 16 layers"),
                        "cuda_graph": graph is not None},
             "roofline": roof,
             "cpu_baseline": cpu,
@@ -692,6 +709,9 @@ def main() -> None:
     ap.add_argument("--chained", action="store_true",
                     help="run the 16 layers as a network (ReLU + max-pool between blocks)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--reuse-depth-inputs", action="store_true",
+                    help="repeated layers (conv3.2 x3 ...) re-run one input and filter set, as "
+                         "the reference's cmd_bench does (default: distinct per instance)")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()
     if args.warmup < 3:
