@@ -6,7 +6,7 @@ Mirrors the ``bench`` and ``accuracy`` commands of the reference CLI
 1 usage / domain error, 2 runtime failure).  Algorithm names are the
 reference's (Winograd names optionally with a GEMM precision suffix,
 ``f4x4-fx:bf16``).  The CLI runs in-process;
-there is no HTTP transport.
+``serve`` runs the HTTP service (service/app.py) under uvicorn.
 """
 from __future__ import annotations
 
@@ -38,12 +38,21 @@ def build_parser() -> argparse.ArgumentParser:
     pa.add_argument("--scale", type=float, default=1.0)
     pa.add_argument("--format", choices=("csv", "text"), default="csv")
     pa.add_argument("--out", metavar="FILE", default=None)
+    ps = sub.add_parser("serve", help="run the HTTP service (uvicorn)")
+    ps.add_argument("--host", default="127.0.0.1")
+    ps.add_argument("--port", type=int, default=8000)
     return p
 
 
 def main(argv: Optional[list] = None) -> int:
     args = build_parser().parse_args(argv)
     from .commands import BENCH_ALGOS, WINOGRAD_ALGOS, cmd_accuracy, cmd_bench
+    if args.command == "serve":  # cli.py `winoconv serve`
+        import uvicorn
+
+        from .service import create_app
+        uvicorn.run(create_app(), host=args.host, port=args.port)
+        return 0
     try:
         if args.command == "accuracy":
             rep = cmd_accuracy(suite=args.suite, algos=[a for a in args.algos.split(",") if a],

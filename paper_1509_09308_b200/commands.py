@@ -61,6 +61,17 @@ def layer_inputs(cfg: LayerConfig, seed: int, index: int) -> Tuple[Tensor4, Tens
 _layer_inputs = layer_inputs
 
 
+def _parse_cell(c: str):
+    if c == "":
+        return None
+    for conv in (int, float):
+        try:
+            return conv(c)
+        except ValueError:
+            pass
+    return c
+
+
 @dataclass
 class Report:
     columns: Tuple[str, ...]
@@ -79,6 +90,32 @@ class Report:
             lines.append(",".join("" if v is None else repr(v) if isinstance(v, float) else str(v)
                                   for v in r))
         return "\n".join(lines) + "\n"
+
+    @classmethod
+    def from_csv(cls, text: str) -> "Report":
+        """Inverse of to_csv (reports.py:65-85): '# seed=' header, empty cells
+        are None, ints and floats (repr round-trips exactly) are parsed back."""
+        import csv
+
+        seed = None
+        lines = []
+        for line in text.splitlines():
+            if line.startswith("#"):
+                body = line.lstrip("#").strip()
+                if body.startswith("seed="):
+                    seed = int(body[len("seed="):])
+                continue
+            if line.strip():
+                lines.append(line)
+        if not lines:
+            raise ValueError("empty report text")
+        parsed = list(csv.reader(lines))
+        rep = cls(columns=tuple(parsed[0]), seed=seed)
+        for raw in parsed[1:]:
+            if len(raw) != len(rep.columns):
+                raise ValueError(f"row {raw!r} does not match header {rep.columns}")
+            rep.rows.append(tuple(_parse_cell(c) for c in raw))
+        return rep
 
     def to_text(self) -> str:
         def fmt(v):
