@@ -803,7 +803,7 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
     }
     tm.mark(2);
     e = launch_output_transform(p->m, p->prec, Mb, y, L.N, L.K, p->th, p->tw, p->oh, p->ow, row0,
-                                Pc, p->m_ld, p->splits, cs, p->m_bf16);
+                                Pc, p->m_ld, p->splits, cs, p->m_bf16, V, p->v_bytes);
     if (e != cudaSuccess) return cuda_fail(e, "output transform");
     tm.mark(3);
   }

@@ -77,9 +77,12 @@ cudaError_t launch_input_transform(int m, int prec, const void* d, void* V, int 
 
 // M [splits][alpha^2][K][m_ld] (float, or double for FP64) -> y (N,K,oh,ow), clipped;
 // split slices are summed in ascending order (deterministic).
+// `dead`/`dead_bytes`: a 128-byte-aligned region (the chunk's V) that is dead once
+// the GEMM has run; the TMA variant drops its L2 lines (no HBM write-back).
 cudaError_t launch_output_transform(int m, int prec, const void* Mbuf, void* y, int N, int K,
                                     int th, int tw, int oh, int ow, int row0, long long Pc,
-                                    long long m_ld, int splits, cudaStream_t s, int m_bf16 = 0);
+                                    long long m_ld, int splits, cudaStream_t s, int m_bf16 = 0,
+                                    const void* dead = nullptr, size_t dead_bytes = 0);
 
 // Whole layer on chip for C <= 8 (input transform + C-term reduction + output
 // transform in one kernel); U in the plan's operand format.

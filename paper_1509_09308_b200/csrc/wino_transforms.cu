@@ -492,7 +492,8 @@ struct OutTma {
 template <int M, typename MT>
 __global__ void __launch_bounds__(kOutTP) output_transform_tma_kernel(
     const __grid_constant__ CUtensorMap tmM, float* __restrict__ y, int K, int th, int tw, int oh,
-    int ow, int row0, long long Pc, const char* __restrict__ mbase, long long m_ld, int discard) {
+    int ow, int row0, long long Pc, const char* __restrict__ mbase, long long m_ld, int discard,
+    const char* __restrict__ dead, long long dead_lines) {
   using A = Alg<M>;
   using Cfg = OutTma<M, MT>;
   constexpr int AL = A::alpha;
@@ -512,6 +513,16 @@ __global__ void __launch_bounds__(kOutTP) output_transform_tma_kernel(
   if (threadIdx.x == 0) {
     ptx::mbar_arrive_expect_tx(&bar, Cfg::bytes);
     ptx::tma_load_3d(s, &tmM, &bar, p0, k0, 0);
+  }
+  if (dead_lines > 0) {
+    // the chunk's V is dead (the GEMM has completed): this block's share of
+    // its 128-byte lines leaves L2 without a write-back, under the box load
+    const long long nb = static_cast<long long>(gridDim.x) * gridDim.y;
+    const long long per = (dead_lines + nb - 1) / nb;
+    const long long l0 = (static_cast<long long>(blockIdx.y) * gridDim.x + blockIdx.x) * per;
+    const long long l1 = min(dead_lines, l0 + per);
+    for (long long l = l0 + threadIdx.x; l < l1; l += kOutTP)
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(dead + 128 * l) : "memory");
   }
   ptx::mbar_wait(&bar, 0);
   if (discard) {
@@ -1004,7 +1015,7 @@ cudaError_t launch_input_transform(int m, int prec, const void* d, void* V, int 
 template <int M, typename MT>
 static cudaError_t output_tma_launch(const void* Mbuf, void* y, int K, int th, int tw, int oh,
                                      int ow, int row0, long long Pc, long long m_ld,
-                                     cudaStream_t s) {
+                                     cudaStream_t s, const void* dead, size_t dead_bytes) {
   using Cfg = OutTma<M, MT>;
   alignas(64) CUtensorMap tmM;
   // M [a2][K][m_ld] (fp32 or bf16), box (128 tiles, OF filters, a2 components), no swizzle
@@ -1024,20 +1035,31 @@ static cudaError_t output_tma_launch(const void* Mbuf, void* y, int K, int th, i
   const dim3 grid(static_cast<unsigned>((Pc + kOutTP - 1) / kOutTP), (K + Cfg::OF - 1) / Cfg::OF);
   static const bool no_discard = getenv("WINO_NO_DISCARD") != nullptr;
   const int discard = !no_discard && m_ld % 64 == 0 && (reinterpret_cast<uintptr_t>(Mbuf) & 127) == 0;
+  // V discard is opt-in (WINO_VDISCARD=1): it takes conv3.2 F4 bf16 N=64 from 432 to
+  // 288 MB of DRAM writes per forward (1.40x the compulsory y) but the pass gets
+  // 1-2% slower (profiles/r2/vdiscard.txt)
+  static const bool vdiscard = !no_discard && getenv("WINO_VDISCARD") != nullptr;
+  const long long dead_lines =
+      (vdiscard && dead && (reinterpret_cast<uintptr_t>(dead) & 127) == 0)
+          ? static_cast<long long>(dead_bytes / 128) : 0;
   launch_k(kern, grid, dim3(kOutTP), static_cast<size_t>(Cfg::bytes + 128), s, tmM,
            static_cast<float*>(y), K, th, tw, oh, ow, row0, Pc,
-           static_cast<const char*>(Mbuf), m_ld, discard);
+           static_cast<const char*>(Mbuf), m_ld, discard, static_cast<const char*>(dead),
+           dead_lines);
   return cudaGetLastError();
 }
 
 cudaError_t launch_output_transform(int m, int prec, const void* Mbuf, void* y, int N, int K,
                                     int th, int tw, int oh, int ow, int row0, long long Pc,
-                                    long long m_ld, int splits, cudaStream_t s, int m_bf16) {
+                                    long long m_ld, int splits, cudaStream_t s, int m_bf16,
+                                    const void* dead, size_t dead_bytes) {
   if (Pc <= 0 || K <= 0) return cudaSuccess;
   if (m_bf16) {  // bf16-staged M (bf16 GEMM, no split-C): TMA path only
     if (splits != 1) return cudaErrorInvalidValue;
-    return m == 2 ? output_tma_launch<2, __nv_bfloat16>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s)
-                  : output_tma_launch<4, __nv_bfloat16>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s);
+    return m == 2 ? output_tma_launch<2, __nv_bfloat16>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s,
+                                                        dead, dead_bytes)
+                  : output_tma_launch<4, __nv_bfloat16>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s,
+                                                        dead, dead_bytes);
   }
   // F(4x4) chunks of <= 256 tiles (conv3-5 at N = 1) take the per-thread
   // kernel: VGG-E F4 fp16 N=1 0.294 -> 0.275 ms.  For F(2x2) the TMA box stays
@@ -1047,8 +1069,10 @@ cudaError_t launch_output_transform(int m, int prec, const void* Mbuf, void* y, 
       getenv("WINO_OUT_TMA_MIN") ? atoll(getenv("WINO_OUT_TMA_MIN")) : 256;
   if (prec != kFP64 && splits == 1 && (m == 2 || Pc > tma_min) &&
       getenv("WINO_NO_TMA_OUTPUT") == nullptr)
-    return m == 2 ? output_tma_launch<2, float>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s)
-                  : output_tma_launch<4, float>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s);
+    return m == 2 ? output_tma_launch<2, float>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s,
+                                                dead, dead_bytes)
+                  : output_tma_launch<4, float>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s,
+                                                dead, dead_bytes);
   const dim3 grid(static_cast<unsigned>((Pc + 127) / 128), K);
   static DeviceOnce configured;
   if (configured.first()) {
