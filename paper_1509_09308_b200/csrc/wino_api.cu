@@ -313,7 +313,13 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
   // extra rounding of M is of the size of the bf16 operand roundings of U and V
   // that already dominate the variant's error (measured +22% rms),
   // and it halves the largest staged tensor.  WINO_M_FP32=1 keeps fp32 M.
-  p->m_es = (prec == kBF16 && getenv("WINO_M_FP32") == nullptr) ? 2 : p->acc_bytes;
+  // fp16 GEMM: M staged as fp16 (scaled by 2^-kM16Shift) -- fp16's 11-bit
+  // significand keeps the variant ~5x tighter than bf16 operands (emulated F4:
+  // 0.77% -> 1.2% of max|y|, bf16 6-7%) at the bf16 plan's staging bytes;
+  // WINO_FP16_M32=1 (or WINO_M_FP32=1) keeps fp32 M.
+  const bool m16 = getenv("WINO_M_FP32") == nullptr &&
+                   (prec == kBF16 || (prec == kFP16 && getenv("WINO_FP16_M32") == nullptr));
+  p->m_es = m16 ? 2 : p->acc_bytes;
   const size_t per_tile = static_cast<size_t>(p->nsplit) * p->a2 * p->c_pad * p->esize +
                           static_cast<size_t>(p->a2) * L.K * p->m_es;
   const size_t per_row = per_tile * p->tw;
@@ -452,7 +458,14 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
     p->overlap = p->num_chunks > 1;
     if (!p->overlap) p->nbuf = 1;
   }
-  p->m_bf16 = (p->m_es == 2 && p->splits == 1 && !p->smallc && p->path == kPathStaged) ? 1 : 0;
+  // (F(4x4) single chunks of <= output_tma_min_tiles() tiles -- conv3-5 at N = 1 --
+  // keep fp32 M: their per-thread output transform beats the TMA box, and the
+  // staging bytes of one small chunk do not matter; F4 fp16 N=1 0.303 -> 0.282 ms)
+  // (WINO_M16_SMALL=1 stages them in 16 bits too, as a multi-chunk plan would)
+  const bool small_f4 = m == 4 && p->num_chunks == 1 && p->chunk_tiles <= output_tma_min_tiles() &&
+                        getenv("WINO_M16_SMALL") == nullptr;
+  p->m_bf16 = (p->m_es == 2 && p->splits == 1 && !p->smallc && p->path == kPathStaged && !small_f4)
+                  ? (prec == kFP16 ? 2 : 1) : 0;
   if (!p->m_bf16) p->m_es = p->acc_bytes;
   // Non-FX 3xTF32 staged plans: the filter transform writes U as hi / lo planes
   // in the workspace, so the GEMM's split warps only split V (into TMEM).
@@ -482,10 +495,10 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
     while (p->splits > 1 && p->nbuf * (p->v_bytes + p->m_bytes) + p->ypart_bytes > workspace_limit) {
       const int kbps = (num_kb + p->splits - 2) / (p->splits - 1);
       p->splits = (num_kb + kbps - 1) / kbps;
-      if (p->splits == 1 && prec == kBF16 && getenv("WINO_M_FP32") == nullptr && !p->smallc &&
+      if (p->splits == 1 && m16 && !p->smallc && !small_f4 &&
           p->path == kPathStaged) {
         p->m_es = 2;
-        p->m_bf16 = 1;
+        p->m_bf16 = prec == kFP16 ? 2 : 1;
       }
       set_m_bytes();
     }

@@ -25,6 +25,7 @@
 #include <cstdlib>
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include "sm100_ptx.cuh"
 #include "wino_internal.h"
@@ -132,7 +133,8 @@ __device__ __forceinline__ void split_region(uint32_t hi, int n, int lo_off, int
 // double-buffered in TMEM (2 x BN columns) so the epilogue of unit j overlaps
 // the MMAs of unit j+1.  Split-C units (small-P layers) write partial sums to
 // separate M slices that the output transform adds in a fixed order.
-// MB: store M as bf16 (the bf16 GEMM's staged M, wino_api.cu planner).
+// MB: store M in 16 bits (bf16 for the bf16 GEMM, fp16 x 2^-kM16Shift for the
+// fp16 GEMM: the staged M of the 16-bit plans, wino_api.cu planner).
 // BS (with TA): U arrives as hi / lo planes (filter transform split2), so the
 // B operand needs no on-chip split; TMA loads both planes into the stage.
 // TRN (3xTF32, K > P layers): roles swapped -- A (M side, split into TMEM) is
@@ -423,12 +425,16 @@ __global__ void __launch_bounds__(gemm_threads<PREC>(), 1)
                          "r"(r[c & 1][4 * c4]), "r"(r[c & 1][4 * c4 + 1]), "r"(r[c & 1][4 * c4 + 2]),
                          "r"(r[c & 1][4 * c4 + 3])
                          : "memory");
-        } else if constexpr (MB) {  // [32 filters][32 tiles] bf16
+        } else if constexpr (MB) {  // [32 filters][32 tiles] bf16, or fp16 x 2^-kM16Shift
           const uint32_t sh = sb - 2 * lane;  // sbuf0 carries 4*lane
 #pragma unroll
           for (int jj = 0; jj < 32; ++jj) {
-            const unsigned short h =
-                __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(r[c & 1][jj])));
+            unsigned short h;
+            if constexpr (PREC == kFP16)
+              h = __half_as_ushort(__float2half_rn(__uint_as_float(r[c & 1][jj]) *
+                                                   (1.0f / (1 << kM16Shift))));
+            else
+              h = __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(r[c & 1][jj])));
             asm volatile("st.shared.b16 [%0], %1;" ::"r"(sh + jj * 64), "h"(h) : "memory");
           }
         } else {
@@ -959,7 +965,7 @@ static cudaError_t launch_prec(const GemmArgs& a, cudaStream_t s) {
       }
     }
   }
-  if constexpr (PREC == kBF16) {
+  if constexpr (PREC == kBF16 || PREC == kFP16) {
     if (a.m_bf16) {
       switch (a.bn) {
         case 32: return launch_tc<PREC, 32, false, true>(a, s);

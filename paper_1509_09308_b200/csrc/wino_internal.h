@@ -77,6 +77,9 @@ cudaError_t launch_input_transform(int m, int prec, const void* d, void* V, int 
 
 // M [splits][alpha^2][K][m_ld] (float, or double for FP64) -> y (N,K,oh,ow), clipped;
 // split slices are summed in ascending order (deterministic).
+// F(4x4) chunks of at most this many tiles take the per-thread output transform
+// (fp32 M) instead of the TMA box (WINO_OUT_TMA_MIN, default 256).
+long long output_tma_min_tiles();
 // `dead`/`dead_bytes`: a 128-byte-aligned region (the chunk's V) that is dead once
 // the GEMM has run; the TMA variant drops its L2 lines (no HBM write-back).
 cudaError_t launch_output_transform(int m, int prec, const void* Mbuf, void* y, int N, int K,
@@ -87,6 +90,10 @@ cudaError_t launch_output_transform(int m, int prec, const void* Mbuf, void* y, 
 // Whole layer on chip for C <= 8 (input transform + C-term reduction + output
 // transform in one kernel); U in the plan's operand format.
 constexpr int kSmallCMax = 8;
+// fp16-staged M holds M * 2^-kM16Shift (exact power of two): |M| up to 2^20 stays
+// finite and |M| >= 2^-10 keeps full fp16 precision (the fp16 operands U, V
+// already bound the data to fp16 range).
+constexpr int kM16Shift = 4;
 cudaError_t launch_fused_smallc(int m, int prec, const void* d, const void* U, void* y, int N,
                                 int C, int H, int W, int K, int pad, int th, int tw, int oh,
                                 int ow, int c_pad, cudaStream_t s);
@@ -120,7 +127,7 @@ struct GemmArgs {
   int bn;          // filters per CTA (tcgen05 N)
   int splits;      // split-C factor: partial sums go to M slices [splits][a2][K][m_ld]
   long long m_ld;  // M row stride (>= Pc, multiple of 4 -- 8 for bf16 M -- for the TMA store)
-  int m_bf16 = 0;  // bf16 GEMM only: M staged as bf16 (see wino_api.cu planner)
+  int m_bf16 = 0;  // 16-bit GEMMs: M staged in 16 bits (1 = bf16, 2 = fp16 x 2^-kM16Shift; planner)
   int b_split = 0; // 3xTF32 only: U holds [hi planes][lo planes] (no on-chip B split)
   int tr = 0;      // 3xTF32 TMEM-A only: filters on the MMA M side, bn = tiles per unit
 };

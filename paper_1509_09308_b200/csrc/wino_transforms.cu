@@ -8,6 +8,8 @@
 #include <cstdlib>
 
 #include "sm100_ptx.cuh"
+#include <type_traits>
+
 #include "wino_internal.h"
 #include "winograd_mats.cuh"
 
@@ -561,7 +563,10 @@ __global__ void __launch_bounds__(kOutTP) output_transform_tma_kernel(
     for (int xi = 0; xi < AL; ++xi)
 #pragma unroll
       for (int nu = 0; nu < AL; ++nu) {
-        if constexpr (sizeof(MT) == 2)
+        if constexpr (std::is_same<MT, __half>::value)
+          in[xi][nu] = __half2float(s[((xi * AL + nu) * Cfg::OF + f) * kOutTP + t]) *
+                       static_cast<float>(1 << kM16Shift);
+        else if constexpr (sizeof(MT) == 2)
           in[xi][nu] = __bfloat162float(s[((xi * AL + nu) * Cfg::OF + f) * kOutTP + t]);
         else
           in[xi][nu] = s[((xi * AL + nu) * Cfg::OF + f) * kOutTP + t];
@@ -1049,11 +1054,23 @@ static cudaError_t output_tma_launch(const void* Mbuf, void* y, int K, int th, i
   return cudaGetLastError();
 }
 
+long long output_tma_min_tiles() {
+  static const long long v = getenv("WINO_OUT_TMA_MIN") ? atoll(getenv("WINO_OUT_TMA_MIN")) : 256;
+  return v;
+}
+
 cudaError_t launch_output_transform(int m, int prec, const void* Mbuf, void* y, int N, int K,
                                     int th, int tw, int oh, int ow, int row0, long long Pc,
                                     long long m_ld, int splits, cudaStream_t s, int m_bf16,
                                     const void* dead, size_t dead_bytes) {
   if (Pc <= 0 || K <= 0) return cudaSuccess;
+  if (m_bf16 == 2) {  // fp16-staged M (x 2^-kM16Shift; fp16 GEMM, no split-C): TMA path only
+    if (splits != 1) return cudaErrorInvalidValue;
+    return m == 2 ? output_tma_launch<2, __half>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s,
+                                                 dead, dead_bytes)
+                  : output_tma_launch<4, __half>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s,
+                                                 dead, dead_bytes);
+  }
   if (m_bf16) {  // bf16-staged M (bf16 GEMM, no split-C): TMA path only
     if (splits != 1) return cudaErrorInvalidValue;
     return m == 2 ? output_tma_launch<2, __nv_bfloat16>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s,
@@ -1065,8 +1082,7 @@ cudaError_t launch_output_transform(int m, int prec, const void* Mbuf, void* y, 
   // kernel: VGG-E F4 fp16 N=1 0.294 -> 0.275 ms.  For F(2x2) the TMA box stays
   // faster on every chunk size in the pass (F2 fp32 N=1: 0.371 vs 0.377 ms).
   // WINO_OUT_TMA_MIN overrides the F(4x4) tile threshold.
-  static const long long tma_min =
-      getenv("WINO_OUT_TMA_MIN") ? atoll(getenv("WINO_OUT_TMA_MIN")) : 256;
+  const long long tma_min = output_tma_min_tiles();
   if (prec != kFP64 && splits == 1 && (m == 2 || Pc > tma_min) &&
       getenv("WINO_NO_TMA_OUTPUT") == nullptr)
     return m == 2 ? output_tma_launch<2, float>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s,

@@ -8,8 +8,8 @@ Tolerances (max-abs, stated per F(m,r) and GEMM precision):
   * vs the reference's fp32 Winograd output: |diff| <= 2e-5 * (1 + max|y|)
     for fp32 (both are fp32-accurate; only summation order differs).
   * reduced-precision GEMMs, relative to max|y|: tf32 <= 1e-2 (F2) / 4e-2 (F4);
-    fp16 <= 4e-3 / 2e-2; bf16 <= 2e-2 / 1.5e-1  (operand rounding of U and V,
-    measured envelope x ~3 margin).
+    fp16 <= 4e-3 / 2.5e-2; bf16 <= 2e-2 / 1.5e-1  (operand rounding of U and V,
+    plus the 16-bit staging of M).
 """
 import numpy as np
 import pytest
@@ -18,7 +18,7 @@ from oracle import winograd_oracle as O
 
 pytestmark = pytest.mark.gpu
 
-REL_TOL = {("tf32", 2): 1e-2, ("tf32", 4): 4e-2, ("fp16", 2): 4e-3, ("fp16", 4): 2e-2,
+REL_TOL = {("tf32", 2): 1e-2, ("tf32", 4): 4e-2, ("fp16", 2): 4e-3, ("fp16", 4): 2.5e-2,
            ("bf16", 2): 2e-2, ("bf16", 4): 1.5e-1}
 
 
@@ -323,11 +323,13 @@ def test_small_c_layer(wb, C):
             assert O.max_abs_error(y64, O.direct_forward(d64, g64, 1)) < 1e-12
 
 
+@pytest.mark.parametrize("prec", ["bf16", "fp16"])
 @pytest.mark.parametrize("m", [2, 4])
-def test_bf16_staged_m_error_budget(wb, monkeypatch, m):
-    """The bf16 GEMM stages M in bf16 (fp32 accumulation, one extra rounding of
-    each accumulator).  Measured on B200 (tools/mbf16_error.py): +22-23% rms
-    and +18-39% max-abs error over fp32-staged M, both inside the bf16 gate.
+def test_bf16_staged_m_error_budget(wb, monkeypatch, m, prec):
+    """The 16-bit GEMMs stage M in 16 bits (fp32 accumulation, one extra
+    rounding of each accumulator: bf16, or fp16 of M * 2^-4).  Measured on
+    B200 (tools/mbf16_error.py): bf16 +22-23% rms and +18-39% max-abs error
+    over fp32-staged M; fp16 (emulated, tools/m16_emulation.py) +23% rms.
     Gates: within REL_TOL, rms error <= 1.35x the fp32-M plan's."""
     import torch
     monkeypatch.setenv("WINO_PATH", "staged")
@@ -336,15 +338,15 @@ def test_bf16_staged_m_error_budget(wb, monkeypatch, m):
     gn = O.fill_uniform((80, 96, 3, 3), 62)
     d, g = torch.from_numpy(dn).cuda(), torch.from_numpy(gn).cuda()
     ref = O.direct_forward(dn, gn, 1)
-    plan = wb.WinogradPlan(cfg, m, "bf16")
+    plan = wb.WinogradPlan(cfg, m, prec)
     assert plan.info["m_bytes_per_elem"] == 2
     e16 = plan.forward(d, g=g).cpu().numpy().astype(np.float64) - ref
     monkeypatch.setenv("WINO_M_FP32", "1")
-    plan32 = wb.WinogradPlan(cfg, m, "bf16")
+    plan32 = wb.WinogradPlan(cfg, m, prec)
     assert plan32.info["m_bytes_per_elem"] == 4
     e32 = plan32.forward(d, g=g).cpu().numpy().astype(np.float64) - ref
     scale = np.abs(ref).max()
-    assert np.abs(e16).max() / scale <= REL_TOL[("bf16", m)]
+    assert np.abs(e16).max() / scale <= REL_TOL[(prec, m)]
     rms16, rms32 = np.sqrt((e16 ** 2).mean()), np.sqrt((e32 ** 2).mean())
     assert rms16 <= 1.35 * rms32, (rms16, rms32)
 

@@ -35,14 +35,15 @@ LAYERS = (("conv1.1", 3, 224, 64), ("conv1.2", 64, 224, 64), ("conv2.1", 64, 112
 # Max-abs error vs the fp64 direct convolution, relative to max|y|, per
 # (m, operand precision), from the envelope measured on B200 over all nine
 # VGG-E shapes at N = 1 and 8 (worst case x ~1.5): tf32 F2 5.4e-4 / F4 9.8e-3,
-# fp16 F2 5.4e-4 / F4 9.8e-3, bf16 F2 5.9e-3 / F4 1.2e-1 (bf16 also stages M in
-# bf16).  fp32 = 3xTF32 is held to the reference's own absolute gates (5e-4 /
+# fp16 F2 7.1e-4 / F4 1.5e-2, bf16 F2 5.9e-3 / F4 1.2e-1 (both 16-bit GEMMs
+# stage M in 16 bits on multi-chunk / > 256-tile F4 plans: bf16, or fp16 of
+# M * 2^-4; fp16 with fp32 M measured F2 5.4e-4 / F4 9.8e-3).  fp32 = 3xTF32 is held to the reference's own absolute gates (5e-4 /
 # 5e-3, test_engine.py:97-112) and to within REF_FACTOR of the reference fp32
 # implementation's own error on the same inputs: tcgen05 accumulates with
 # truncation, so the staged GEMM's error grows with the channel count (measured
 # up to 2.9x the reference's at C = 512 on one channel split; 0.3-1.4x at C <=
 # 128; the fused path, and split-C plans, sit at or below the reference).
-REL_GATE = {(2, "tf32"): 1e-3, (4, "tf32"): 1.5e-2, (2, "fp16"): 1e-3, (4, "fp16"): 1.5e-2,
+REL_GATE = {(2, "tf32"): 1e-3, (4, "tf32"): 1.5e-2, (2, "fp16"): 1.2e-3, (4, "fp16"): 2.5e-2,
             (2, "bf16"): 1e-2, (4, "bf16"): 1.5e-1}
 ABS_GATE_FP32 = {2: 5e-4, 4: 5e-3}
 REF_FACTOR = 4.0
@@ -215,7 +216,7 @@ def _batch(i, N):
     (16, "bf16", 4), (16, "tf32", 4), (32, "bf16", 4), (32, "tf32", 4),
 ])
 @pytest.mark.parametrize("i", [1, 3, 5, 7, 8])
-def test_batched_plans_image0_and_slices(wb, fx, i, N, prec, m):
+def test_batched_plans_image0_and_slices(wb, fx, monkeypatch, i, N, prec, m):
     """config 3 batch sizes: image 0 against the reference fixture / fp64
     direct, image N-1 against a single-image plan of the same precision
     (chunking, split-C and stream overlap must not change any image)."""
@@ -223,6 +224,9 @@ def test_batched_plans_image0_and_slices(wb, fx, i, N, prec, m):
     lbl, C, H, K = LAYERS[i]
     if N * C * H * H > 64 * 512 * 112 * 112:
         pytest.skip("input > 1.6 GB")
+    # a single small F(4x4) chunk keeps fp32 M by default; stage M in 16 bits in
+    # both plans so that only chunking and ordering differ between them
+    monkeypatch.setenv("WINO_M16_SMALL", "1")
     d, g, y64 = _batch(i, N)
     cfg = wb.LayerConfig(N=N, C=C, H=H, W=H, K=K, pad=1)
     plan, y = _run(wb, cfg, m, prec, d, g)
