@@ -681,11 +681,12 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
                  cudaStreamWaitEvent(side->st, side->fork, 0) != cudaSuccess))
       side = nullptr;
   }
-  // Single-chunk staged plans whose filter transform outweighs the input
-  // transform (K > P: the deep, small-image layers at small N) swap the two:
-  // the input transform goes to the side stream and the filter transform stays
-  // in-stream, so the GEMM launches programmatically (PDL) behind the longer of
-  // the two instead of behind an event join.
+  // WINO_SIDE_SWAP=1: single-chunk staged plans with K > P swap the two, the
+  // input transform on the side stream and the filter transform in-stream.
+  // That was faster while the filter transform was the longer of the two; since
+  // those plans' input transform writes V as tf32 hi / lo planes it is the
+  // longer one, and keeping it in-stream (the GEMM launches behind it by PDL)
+  // measured 0.3731 -> 0.3690 ms on VGG-E F2 fp32 N=1.
   bool input_enqueued = false;  // chunk 0's input transform already launched
   const bool u_split = !U && p->u_split2;  // U computed here as hi / lo planes
   if (combined) {
@@ -698,8 +699,9 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
     U = ws;
     ws += p->u_ws;
   } else if (!U) {
+    static const bool swap = getenv("WINO_SIDE_SWAP") != nullptr;
     const bool in_side = side && p->path == kPathStaged && p->num_chunks == 1 &&
-                         !chunk_overlap && static_cast<long long>(p->L.K) > p->P;
+                         !chunk_overlap && static_cast<long long>(p->L.K) > p->P && swap;
     if (in_side) {
       input_enqueued = true;
       cudaError_t e = launch_input_transform(p->m, p->v_split2 ? kFP32S : p->prec, d, ws + p->u_ws, p->L.N, p->L.C,
