@@ -19,7 +19,11 @@ algo, prec, batch = sys.argv[1], sys.argv[2], int(sys.argv[3])
 out = sys.argv[4] if len(sys.argv) > 4 else None
 m, fx, _ = wb.parse_algo(algo)
 layers = []
-for (lbl, C, H, K, depth) in VGG_E_ROWS:
+rows = list(VGG_E_ROWS)
+if os.environ.get("TL_ROTATE"):  # diagnostic: start the pass at another layer
+    k = int(os.environ["TL_ROTATE"])
+    rows = rows[k:] + rows[:k]
+for (lbl, C, H, K, depth) in rows:
     cfg = wb.LayerConfig(N=batch, C=C, H=H, W=H, K=K, pad=1)
     plan = wb.WinogradPlan(cfg, m, prec)
     d = torch.rand((batch, C, H, H), device="cuda") * 2 - 1
