@@ -4,6 +4,7 @@
 # default workload, ncu --set full of its dominant kernel (conv4.2 GEMM).
 set -u
 OUT=gpurun_out/$1; mkdir -p $OUT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/smi.txt
 T="timeout -s KILL"
 $T 400 python bench.py > $OUT/bench_default.json 2> $OUT/bench_default.err
 for a in "f4x4 fp16 1" "f4x4 fp16 8" "f4x4 fp16 64" "f4x4 bf16 1" "f4x4 bf16 8" "f4x4 bf16 64" "f4x4 tf32 8" "f4x4 tf32 64" "f2x2 fp32 64"; do
