@@ -458,3 +458,73 @@ def test_transposed_gemm_k_gt_p(wb, monkeypatch, m, N, C, H, K, vsplit):
     monkeypatch.setenv("WINO_NO_GEMM_TR", "1")
     y2 = wb.WinogradPlan(cfg, m, "fp32").forward(dd, g=gg).cpu().numpy()
     assert err <= 1.25 * O.max_abs_error(y2, ref) + 1e-6 * (1 + np.abs(ref).max())
+
+
+# ---- winograd_grad_inputs (engine.py:257-275): the reference's TestGradInputs
+# cases (test_engine.py:183-223) through the CUDA path, plus VGG-size layers.
+def _grad_inputs_ref(dy, g, pad):
+    """fp64 dL/dInput: correlation of dY with the flipped, (k,c)-swapped filters."""
+    import torch
+    flipped = torch.from_numpy(np.ascontiguousarray(
+        g[:, :, ::-1, ::-1].transpose(1, 0, 2, 3))).double()
+    return torch.nn.functional.conv2d(torch.from_numpy(dy).double(), flipped,
+                                      padding=2 - pad).numpy()
+
+
+def test_grad_inputs_zero_dy_exact(wb):
+    cfg = wb.LayerConfig(N=1, C=2, H=6, W=6, K=3, pad=1)
+    dy = wb.Tensor4.zeros((1, 3, 6, 6))
+    g = wb.Tensor4.from_array(O.fill_uniform((3, 2, 3, 3), 1))
+    for m in (2, 4):
+        assert np.all(wb.winograd_grad_inputs(dy, g, cfg, wb.builtin(m, 3)).data == 0.0)
+
+
+def test_grad_inputs_center_impulse_identity(wb):
+    cfg = wb.LayerConfig(N=1, C=1, H=6, W=6, K=1, pad=1)
+    g = np.zeros((1, 1, 3, 3))
+    g[0, 0, 1, 1] = 1.0
+    dy = O.fill_uniform((1, 1, 6, 6), 2).astype(np.float64)
+    T = wb.Tensor4.from_array
+    dd = wb.winograd_grad_inputs(T(dy, wb.Precision.FP64), T(g, wb.Precision.FP64), cfg,
+                                 wb.builtin(2, 3)).data
+    np.testing.assert_allclose(dd, dy, atol=1e-12)
+
+
+@pytest.mark.parametrize("m", [2, 4])
+def test_grad_inputs_matches_direct(wb, m):
+    T = wb.Tensor4.from_array
+    # fp64 (test_engine.py:201-207) and fp32 (test_engine.py:209-215) shapes
+    cfg = wb.LayerConfig(N=1, C=1, H=8, W=8, K=1, pad=1)
+    dy = O.fill_uniform((1, 1, 8, 8), 3).astype(np.float64)
+    g = O.fill_uniform((1, 1, 3, 3), 4).astype(np.float64)
+    dd = wb.winograd_grad_inputs(T(dy, wb.Precision.FP64), T(g, wb.Precision.FP64), cfg,
+                                 wb.builtin(m, 3)).data
+    assert O.max_abs_error(dd, _grad_inputs_ref(dy, g, 1)) < 1e-10
+    cfg = wb.LayerConfig(N=2, C=3, H=9, W=7, K=4, pad=1)
+    dy = O.fill_uniform((2, 4, 9, 7), 5)
+    g = O.fill_uniform((4, 3, 3, 3), 6)
+    dd = wb.winograd_grad_inputs(T(dy), T(g), cfg, wb.builtin(m, 3)).data
+    assert O.max_abs_error(dd, _grad_inputs_ref(dy, g, 1)) < 1e-3
+
+
+def test_grad_inputs_pad_too_large(wb):
+    cfg = wb.LayerConfig(N=1, C=1, H=6, W=6, K=1, pad=3)
+    dy = wb.Tensor4.from_array(O.fill_uniform((1, 1, cfg.out_h, cfg.out_w), 7))
+    g = wb.Tensor4.from_array(O.fill_uniform((1, 1, 3, 3), 8))
+    with pytest.raises(ValueError):
+        wb.winograd_grad_inputs(dy, g, cfg, wb.builtin(2, 3))
+
+
+@pytest.mark.parametrize("m", [2, 4])
+@pytest.mark.parametrize("C,H,K,pad", [(256, 56, 256, 1), (512, 14, 512, 1), (64, 30, 96, 0),
+                                       (128, 28, 64, 2)])
+def test_grad_inputs_vgg_size(wb, m, C, H, K, pad):
+    """VGG-size layers (the deep and small-C-out shapes, pad 0 / 1 / 2) against the
+    fp64 gradient, at the fp32 forward gates."""
+    T = wb.Tensor4.from_array
+    cfg = wb.LayerConfig(N=1, C=C, H=H, W=H, K=K, pad=pad)
+    dy = O.fill_uniform((1, K, cfg.out_h, cfg.out_w), 11)
+    g = O.fill_uniform((K, C, 3, 3), 12)
+    dd = wb.winograd_grad_inputs(T(dy), T(g), cfg, wb.builtin(m, 3)).data
+    assert dd.shape == (1, C, H, H)
+    assert O.max_abs_error(dd, _grad_inputs_ref(dy, g, pad)) < (5e-4 if m == 2 else 5e-3)
