@@ -510,11 +510,17 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
 
 // Non-FX forwards of this plan launch the filter and input transforms as one
 // kernel (staged, single chunk, 16-bit operands, TMA-eligible input).
+// Only small layers (P <= 64 tiles: conv4-5 at N = 1) combine the transforms:
+// on larger ones the separate kernels on two streams finish first (VGG-E F4
+// fp16 N=1 0.2834 -> 0.2779 ms, N=8 0.611 -> 0.605 ms against combining every
+// single-chunk 16-bit plan).  WINO_COMBINED_MAXP overrides the tile bound.
 static bool plan_combines_transforms(const wino_plan_s* p) {
   static const bool fp32 = getenv("WINO_FP32_COMBINED") != nullptr;
+  static const long long maxp =
+      getenv("WINO_COMBINED_MAXP") ? atoll(getenv("WINO_COMBINED_MAXP")) : 64;
   return p->path == kPathStaged && !p->smallc &&
          (p->prec == kBF16 || p->prec == kFP16 || (fp32 && p->prec == kFP32)) &&
-         p->num_chunks == 1 && transforms_combinable(p->prec, p->L.W, p->L.pad);
+         p->num_chunks == 1 && p->P <= maxp && transforms_combinable(p->prec, p->L.W, p->L.pad);
 }
 
 int wino_plan_destroy(wino_plan_t plan) {

@@ -935,6 +935,16 @@ cudaError_t launch_transforms(int m, int prec, const void* d, void* V, int N, in
 #undef WINO_TP
 }
 
+// The whole-plane input transform needs enough blocks (images x channel
+// groups) to spread; below 32 the tile-row kernel is faster (conv5 at N = 1:
+// 16 blocks).  At N = 8 (64 blocks) the plane kernel wins: VGG-E F4 fp16 N=8
+// 0.611 -> 0.598 ms, F2 fp32 N=8 1.529 -> 1.513 ms (the bound was 148).
+static long long plane_min_blocks() {
+  static const long long v =
+      getenv("WINO_PLANE_MIN_BLOCKS") ? atoll(getenv("WINO_PLANE_MIN_BLOCKS")) : 32;
+  return v;
+}
+
 template <int M, int PREC>
 static cudaError_t input_one(const void* d, void* V, int N, int C, int H, int W, int pad, int th,
                              int tw, int row0, int rows, long long Pc, int c_pad,
@@ -962,7 +972,7 @@ static cudaError_t input_one(const void* d, void* V, int N, int C, int H, int W,
                              ((C + CB - 1) / CB);
     // enough blocks to cover the SMs (else the tile-row kernel spreads wider)
     if (hw % 4 == 0 && psmem <= 100 * 1024 && (reinterpret_cast<uintptr_t>(d) & 15) == 0 &&
-        (blocks >= 148 || getenv("WINO_FORCE_PLANE_INPUT") != nullptr) &&
+        (blocks >= plane_min_blocks() || getenv("WINO_FORCE_PLANE_INPUT") != nullptr) &&
         getenv("WINO_NO_PLANE_INPUT") == nullptr) {
       auto kp = input_transform_plane_kernel<M, PREC, CPL>;
       static DeviceOnce pconf;
