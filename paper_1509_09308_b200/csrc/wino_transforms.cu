@@ -633,13 +633,17 @@ static void filter_launch(const void* g, void* U, int K, int C, int c_pad, cudaS
   using T = typename OpStore<PREC>::T;
   const long long n = static_cast<long long>(K) * C;
   static const int fpt_env = getenv("WINO_FILTER_FPT") ? atoi(getenv("WINO_FILTER_FPT")) : 0;
-  // Four (k,c) per thread (two for fp64).  Alone on the GPU one per thread is
-  // twice as fast (512 x 512 F2 fp32: 4.1 vs 8.3 us), but in the pass the
-  // transform runs beside the input transform or just ahead of the GEMM, whose
-  // CTAs launch early (PDL) and co-reside only while the transform leaves SMs
-  // free: VGG-E F2 fp32 N=1 0.380 ms at four per thread vs 0.397 at one.
-  const int fpt = fpt_env == 1 || fpt_env == 2 || fpt_env == 4 ? fpt_env
-                                                               : (sizeof(T) == 4 ? 4 : 2);
+  // (k,c) pairs per thread.  Alone on the GPU one per thread is twice as fast
+  // (512 x 512 F2 fp32: 4.1 vs 8.3 us).  For the 3xTF32 plans four stay faster
+  // in the pass, where the transform runs beside the input transform or just
+  // ahead of the GEMM, whose CTAs launch early (PDL) and co-reside only while
+  // the transform leaves SMs free: VGG-E F2 fp32 N=1 0.380 ms at four per
+  // thread vs 0.397 at one.  For the single-pass GEMMs (tf32 / bf16 / fp16) one
+  // per thread measured faster: F4 tf32 N=8 0.859 -> 0.819 ms, N=1 0.336 ->
+  // 0.325; F4 bf16 N=8 0.589 -> 0.577; F4 fp16 N=8 0.593 -> 0.580.  fp64: two.
+  const int fpt = fpt_env == 1 || fpt_env == 2 || fpt_env == 4
+                      ? fpt_env
+                      : (PREC == kFP32 ? 4 : PREC == kFP64 ? 2 : 1);
   auto go = [&](auto kern, int FPT) {
     max_carveout(kern);
     launch_k(kern, dim3(static_cast<unsigned>((n + 256 * FPT - 1) / (256 * FPT))), dim3(256), 0, s,
