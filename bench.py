@@ -590,7 +590,8 @@ def run_chained(args) -> None:
     if fx:
         raise SystemExit("--chained runs the non-FX forward (filters transformed every step)")
     B = args.batch
-    net = VGGEStack(B, m, prec, seed=0, workspace_limit=args.workspace)
+    net = VGGEStack(B, m, prec, seed=0, workspace_limit=args.workspace,
+                    fuse_act=not args.no_fuse_act)
     gen = torch.Generator(device="cpu").manual_seed(1234 + rank)
     x_host = (torch.rand(net.in_shape, generator=gen) * 2 - 1).pin_memory()
     x = x_host.to(dev)
@@ -673,7 +674,9 @@ def run_chained(args) -> None:
                        "algo": args.algo, "global_batch": B * world, "batch_per_gpu": B,
                        "parallelism": f"dp{world} batch-shard (no collective)",
                        "l2": f"flushed between timed steps ({args.flush_mb} MB write)",
-                       "cuda_graph": True, "chained": True},
+                       "cuda_graph": True, "chained": True,
+                       "relu_pool": "separate pass" if args.no_fuse_act else
+                       "fused into the output transform (wino_forward_act)"},
             "roofline": roof,
             "cpu_baseline": None,
             "e2e": {"value": e2e_val, "unit": "TFLOPS",
@@ -706,6 +709,8 @@ def main() -> None:
                          "(default: --batch images per GPU, weak scaling)")
     ap.add_argument("--flush-mb", type=int, default=256)
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-fuse-act", action="store_true",
+                    help="--chained: ReLU / max-pool as a separate pass, not in the output transform")
     ap.add_argument("--chained", action="store_true",
                     help="run the 16 layers as a network (ReLU + max-pool between blocks)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

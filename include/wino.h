@@ -162,6 +162,18 @@ int wino_fft_forward(const wino_layer_t* layer, int prec, int tile, const void* 
                      const double* g, void* y, void* workspace, size_t workspace_bytes,
                      void* stream);
 
+/* wino_forward with an activation fused into the output transform's stores
+ * (not on the reference's path; the chained VGG-E stack uses it):
+ * WINO_ACT_NONE, WINO_ACT_RELU (y = max(conv, 0)), or WINO_ACT_RELU_POOL
+ * (y = 2x2 / stride-2 max-pool of max(conv, 0): y is (N, K, out_h/2, out_w/2),
+ * out_h and out_w even).  Staged path (and the small-C layer) only:
+ * WINO_EUNSUPPORTED on the fused / hybrid paths. */
+#define WINO_ACT_NONE 0
+#define WINO_ACT_RELU 1
+#define WINO_ACT_RELU_POOL 2
+int wino_forward_act(wino_plan_t plan, const void* d, const void* U, const void* g, void* y,
+                     void* workspace, size_t workspace_bytes, int act, void* stream);
+
 /* Chaining glue for the VGG-E conv stack (network.py; not on the reference's
  * path): y = relu(x), or relu(maxpool2x2(x)) with pool != 0 (H, W even;
  * y is (N,C,H/2,W/2)).  fp32 device pointers, enqueued on `stream`. */

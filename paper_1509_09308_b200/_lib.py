@@ -25,7 +25,7 @@ EXPORTED = ("wino_plan_create", "wino_plan_destroy", "wino_plan_get_info",
             "wino_filter_transform", "wino_forward", "wino_forward_host", "wino_forward_timed",
             "wino_timer_create", "wino_timer_destroy", "wino_timer_break", "wino_timer_read",
             "wino_wgrad_workspace", "wino_grad_weights", "wino_direct_forward", "wino_relu_pool",
-            "wino_fft_workspace", "wino_fft_forward",
+            "wino_fft_workspace", "wino_fft_forward", "wino_forward_act",
             "wino_last_error", "wino_version")
 
 
@@ -87,6 +87,7 @@ def _load() -> ctypes.CDLL:
     lib.wino_fft_forward.argtypes = [ctypes.POINTER(LayerDesc), c_int, c_int, vp, vp, vp, vp, sz,
                                      vp]
     lib.wino_relu_pool.argtypes = [vp, vp, c_int, c_int, c_int, c_int, c_int, vp]
+    lib.wino_forward_act.argtypes = [vp, vp, vp, vp, vp, vp, sz, c_int, vp]
     lib.wino_last_error.restype = ctypes.c_char_p
     lib.wino_version.restype = ctypes.c_char_p
     for name in EXPORTED:

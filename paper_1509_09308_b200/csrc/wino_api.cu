@@ -652,11 +652,23 @@ SideStream* side_stream(cudaStream_t user) {
 
 static int forward_impl(wino_plan_t p, const void* d, const void* U, const void* g, void* y,
                         void* workspace, size_t workspace_bytes, void* stream,
-                        wino_timer_s* timer) {
+                        wino_timer_s* timer, int act = kActNone) {
   g_err.clear();
   if (!p || !d || !y || (!U && !g) || !workspace) {
     set_error("null argument");
     return WINO_EINVAL;
+  }
+  if (act != kActNone && act != kActRelu && act != kActReluPool) {
+    set_error("unknown activation %d", act);
+    return WINO_EINVAL;
+  }
+  if (act == kActReluPool && (p->oh % 2 != 0 || p->ow % 2 != 0)) {
+    set_error("2x2 max-pool needs an even output size, got %dx%d", p->oh, p->ow);
+    return WINO_EINVAL;
+  }
+  if (act != kActNone && !p->smallc && p->path != kPathStaged) {
+    set_error("the activation epilogue runs on the staged path (WINO_PATH=staged)");
+    return WINO_EUNSUPPORTED;
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   StageTimer tm(s, timer);
@@ -749,7 +761,7 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
   const wino_layer_t& L = p->L;
   if (p->smallc) {
     cudaError_t e = launch_fused_smallc(p->m, p->prec, d, U, y, L.N, L.C, L.H, L.W, L.K, L.pad,
-                                        p->th, p->tw, p->oh, p->ow, p->c_pad, s);
+                                        p->th, p->tw, p->oh, p->ow, p->c_pad, s, act);
     if (e != cudaSuccess) return cuda_fail(e, "fused small-C layer");
     tm.mark(1);
     return WINO_OK;
@@ -824,7 +836,7 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
     }
     tm.mark(2);
     e = launch_output_transform(p->m, p->prec, Mb, y, L.N, L.K, p->th, p->tw, p->oh, p->ow, row0,
-                                Pc, p->m_ld, p->splits, cs, p->m_bf16, V, p->v_bytes);
+                                Pc, p->m_ld, p->splits, cs, p->m_bf16, V, p->v_bytes, act);
     if (e != cudaSuccess) return cuda_fail(e, "output transform");
     tm.mark(3);
   }
@@ -843,6 +855,11 @@ static int forward_impl(wino_plan_t p, const void* d, const void* U, const void*
 int wino_forward(wino_plan_t p, const void* d, const void* U, const void* g, void* y,
                  void* workspace, size_t workspace_bytes, void* stream) {
   return forward_impl(p, d, U, g, y, workspace, workspace_bytes, stream, nullptr);
+}
+
+int wino_forward_act(wino_plan_t p, const void* d, const void* U, const void* g, void* y,
+                     void* workspace, size_t workspace_bytes, int act, void* stream) {
+  return forward_impl(p, d, U, g, y, workspace, workspace_bytes, stream, nullptr, act);
 }
 
 int wino_timer_create(wino_timer_t* out) {

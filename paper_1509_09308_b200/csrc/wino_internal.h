@@ -82,10 +82,14 @@ cudaError_t launch_input_transform(int m, int prec, const void* d, void* V, int 
 long long output_tma_min_tiles();
 // `dead`/`dead_bytes`: a 128-byte-aligned region (the chunk's V) that is dead once
 // the GEMM has run; the TMA variant drops its L2 lines (no HBM write-back).
+// `act`: epilogue activation of the written tiles (kActNone / kActRelu /
+// kActReluPool: y is then (N, K, oh/2, ow/2)); see emit_tile.
+enum : int { kActNone = 0, kActRelu = 1, kActReluPool = 2 };
 cudaError_t launch_output_transform(int m, int prec, const void* Mbuf, void* y, int N, int K,
                                     int th, int tw, int oh, int ow, int row0, long long Pc,
                                     long long m_ld, int splits, cudaStream_t s, int m_bf16 = 0,
-                                    const void* dead = nullptr, size_t dead_bytes = 0);
+                                    const void* dead = nullptr, size_t dead_bytes = 0,
+                                    int act = kActNone);
 
 // Whole layer on chip for C <= 8 (input transform + C-term reduction + output
 // transform in one kernel); U in the plan's operand format.
@@ -96,7 +100,7 @@ constexpr int kSmallCMax = 8;
 constexpr int kM16Shift = 4;
 cudaError_t launch_fused_smallc(int m, int prec, const void* d, const void* U, void* y, int N,
                                 int C, int H, int W, int K, int pad, int th, int tw, int oh,
-                                int ow, int c_pad, cudaStream_t s);
+                                int ow, int c_pad, cudaStream_t s, int act = kActNone);
 
 // Weight gradient F(3x3,2x2) (engine.py:278-328): transforms of tiles
 // [b0, b0+nb) into Uw [nsplit][16][K][b_pad] and Vw [nsplit][16][C][b_pad]

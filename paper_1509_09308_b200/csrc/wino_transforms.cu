@@ -72,6 +72,45 @@ struct OpStore<kFP64> {
 template <int M, typename TA>
 __device__ __forceinline__ void store_tile(TA* dst, int ow, int vr, int vc, const TA (&out)[M][M]);
 
+// Write one output tile of (n, k) at tile (ty, tx) with the forward's epilogue
+// activation (wino_forward_act; the chained network's ReLU and 2x2 max-pool,
+// fused here instead of a separate pass over y): kActNone stores the tile,
+// kActRelu stores max(x, 0), kActReluPool stores the 2x2 / stride-2 max of
+// max(x, 0) into y (N, K, oh/2, ow/2).  Tile origins are multiples of m (even)
+// and oh, ow are even, so a tile holds whole pooling windows and its valid rows
+// / columns are even.
+template <int M, typename TA>
+__device__ __forceinline__ void emit_tile(TA* __restrict__ y, int act, int n, int K, int k,
+                                          int oh, int ow, int ty, int tx, int vr, int vc,
+                                          TA (&out)[M][M]) {
+  if (act == kActReluPool) {
+    constexpr int P = M / 2;
+    TA pooled[P][P];
+#pragma unroll
+    for (int i = 0; i < P; ++i)
+#pragma unroll
+      for (int j = 0; j < P; ++j) {
+        const TA a = out[2 * i][2 * j] > out[2 * i][2 * j + 1] ? out[2 * i][2 * j] : out[2 * i][2 * j + 1];
+        const TA b = out[2 * i + 1][2 * j] > out[2 * i + 1][2 * j + 1] ? out[2 * i + 1][2 * j]
+                                                                         : out[2 * i + 1][2 * j + 1];
+        const TA v = a > b ? a : b;
+        pooled[i][j] = v < TA(0) ? TA(0) : v;
+      }
+    const int ph = oh >> 1, pw = ow >> 1;
+    TA* dst = y + ((static_cast<size_t>(n) * K + k) * ph + P * ty) * pw + P * tx;
+    store_tile<P>(dst, pw, vr >> 1, vc >> 1, pooled);
+    return;
+  }
+  if (act == kActRelu) {
+#pragma unroll
+    for (int i = 0; i < M; ++i)
+#pragma unroll
+      for (int j = 0; j < M; ++j) out[i][j] = out[i][j] < TA(0) ? TA(0) : out[i][j];
+  }
+  TA* dst = y + ((static_cast<size_t>(n) * K + k) * oh + M * ty) * ow + M * tx;
+  store_tile<M>(dst, ow, vr, vc, out);
+}
+
 // ============================================================ filter transform
 // Block = 256 x FPT consecutive (k, c) pairs = contiguous 3x3 filters, staged through shared memory with coalesced 16-byte loads (all
 // of a thread's loads in flight at once; the 36-byte records would otherwise
@@ -442,7 +481,8 @@ __global__ void __launch_bounds__(128, 8) output_transform_kernel(const TA* __re
                                                                TA* __restrict__ y, int N, int K,
                                                                int th, int tw, int oh, int ow,
                                                                int row0, long long Pc,
-                                                               long long m_ld, int splits) {
+                                                               long long m_ld, int splits,
+                                                               int act) {
   using A = Alg<M>;
   constexpr int AL = A::alpha;
   const long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -473,8 +513,7 @@ __global__ void __launch_bounds__(128, 8) output_transform_kernel(const TA* __re
   const int rest = static_cast<int>(gp - n * per_img);
   const int ty = rest / tw, tx = rest - ty * tw;
   const int vr = min(M, oh - M * ty), vc = min(M, ow - M * tx);
-  TA* dst = y + ((static_cast<size_t>(n) * K + k) * oh + M * ty) * ow + M * tx;
-  store_tile<M>(dst, ow, vr, vc, out);
+  emit_tile<M>(y, act, n, K, k, oh, ow, ty, tx, vr, vc, out);
 }
 
 // TMA-staged variant (fp32, no split-C): one 3D TMA box brings a block's
@@ -495,7 +534,7 @@ template <int M, typename MT>
 __global__ void __launch_bounds__(kOutTP) output_transform_tma_kernel(
     const __grid_constant__ CUtensorMap tmM, float* __restrict__ y, int K, int th, int tw, int oh,
     int ow, int row0, long long Pc, const char* __restrict__ mbase, long long m_ld, int discard,
-    const char* __restrict__ dead, long long dead_lines) {
+    const char* __restrict__ dead, long long dead_lines, int act) {
   using A = Alg<M>;
   using Cfg = OutTma<M, MT>;
   constexpr int AL = A::alpha;
@@ -573,8 +612,7 @@ __global__ void __launch_bounds__(kOutTP) output_transform_tma_kernel(
       }
     float out[M][M];
     at_2d<M, float>(in, out);
-    float* dst = y + ((static_cast<size_t>(n) * K + k) * oh + M * ty) * ow + M * tx;
-    store_tile<M>(dst, ow, vr, vc, out);
+    emit_tile<M>(y, act, n, K, k, oh, ow, ty, tx, vr, vc, out);
   }
 }
 
@@ -1034,7 +1072,8 @@ cudaError_t launch_input_transform(int m, int prec, const void* d, void* V, int 
 template <int M, typename MT>
 static cudaError_t output_tma_launch(const void* Mbuf, void* y, int K, int th, int tw, int oh,
                                      int ow, int row0, long long Pc, long long m_ld,
-                                     cudaStream_t s, const void* dead, size_t dead_bytes) {
+                                     cudaStream_t s, const void* dead, size_t dead_bytes,
+                                     int act) {
   using Cfg = OutTma<M, MT>;
   alignas(64) CUtensorMap tmM;
   // M [a2][K][m_ld] (fp32 or bf16), box (128 tiles, OF filters, a2 components), no swizzle
@@ -1064,7 +1103,7 @@ static cudaError_t output_tma_launch(const void* Mbuf, void* y, int K, int th, i
   launch_k(kern, grid, dim3(kOutTP), static_cast<size_t>(Cfg::bytes + 128), s, tmM,
            static_cast<float*>(y), K, th, tw, oh, ow, row0, Pc,
            static_cast<const char*>(Mbuf), m_ld, discard, static_cast<const char*>(dead),
-           dead_lines);
+           dead_lines, act);
   return cudaGetLastError();
 }
 
@@ -1076,21 +1115,21 @@ long long output_tma_min_tiles() {
 cudaError_t launch_output_transform(int m, int prec, const void* Mbuf, void* y, int N, int K,
                                     int th, int tw, int oh, int ow, int row0, long long Pc,
                                     long long m_ld, int splits, cudaStream_t s, int m_bf16,
-                                    const void* dead, size_t dead_bytes) {
+                                    const void* dead, size_t dead_bytes, int act) {
   if (Pc <= 0 || K <= 0) return cudaSuccess;
   if (m_bf16 == 2) {  // fp16-staged M (x 2^-kM16Shift; fp16 GEMM, no split-C): TMA path only
     if (splits != 1) return cudaErrorInvalidValue;
     return m == 2 ? output_tma_launch<2, __half>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s,
-                                                 dead, dead_bytes)
+                                                 dead, dead_bytes, act)
                   : output_tma_launch<4, __half>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s,
-                                                 dead, dead_bytes);
+                                                 dead, dead_bytes, act);
   }
   if (m_bf16) {  // bf16-staged M (bf16 GEMM, no split-C): TMA path only
     if (splits != 1) return cudaErrorInvalidValue;
     return m == 2 ? output_tma_launch<2, __nv_bfloat16>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s,
-                                                        dead, dead_bytes)
+                                                        dead, dead_bytes, act)
                   : output_tma_launch<4, __nv_bfloat16>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s,
-                                                        dead, dead_bytes);
+                                                        dead, dead_bytes, act);
   }
   // F(4x4) chunks of <= 256 tiles (conv3-5 at N = 1) take the per-thread
   // kernel: VGG-E F4 fp16 N=1 0.294 -> 0.275 ms.  For F(2x2) the TMA box stays
@@ -1100,9 +1139,9 @@ cudaError_t launch_output_transform(int m, int prec, const void* Mbuf, void* y, 
   if (prec != kFP64 && splits == 1 && (m == 2 || Pc > tma_min) &&
       getenv("WINO_NO_TMA_OUTPUT") == nullptr)
     return m == 2 ? output_tma_launch<2, float>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s,
-                                                dead, dead_bytes)
+                                                dead, dead_bytes, act)
                   : output_tma_launch<4, float>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s,
-                                                dead, dead_bytes);
+                                                dead, dead_bytes, act);
   const dim3 grid(static_cast<unsigned>((Pc + 127) / 128), K);
   static DeviceOnce configured;
   if (configured.first()) {
@@ -1115,11 +1154,11 @@ cudaError_t launch_output_transform(int m, int prec, const void* Mbuf, void* y, 
   if (prec == kFP64) {
     launch_k(m == 2 ? output_transform_kernel<2, double> : output_transform_kernel<4, double>, grid,
              dim3(128), 0, s, static_cast<const double*>(Mbuf), static_cast<double*>(y), N, K, th,
-             tw, oh, ow, row0, Pc, m_ld, splits);
+             tw, oh, ow, row0, Pc, m_ld, splits, act);
   } else {
     launch_k(m == 2 ? output_transform_kernel<2, float> : output_transform_kernel<4, float>, grid,
              dim3(128), 0, s, static_cast<const float*>(Mbuf), static_cast<float*>(y), N, K, th,
-             tw, oh, ow, row0, Pc, m_ld, splits);
+             tw, oh, ow, row0, Pc, m_ld, splits, act);
   }
   return cudaGetLastError();
 }
@@ -1185,7 +1224,7 @@ template <int M, typename T, int CE>
 __global__ void __launch_bounds__(256, 2) fused_smallc_kernel(
     const T* __restrict__ d, const void* __restrict__ U, T* __restrict__ y, int prec, int C,
     int H, int W, int K, int pad, int th, int tw, int oh, int ow, int c_pad, int n_units,
-    int nkc) {
+    int nkc, int act) {
   using A = Alg<M>;
   using Cfg = SmallCfg<M, T>;
   constexpr int AL = Cfg::AL, A2 = Cfg::A2, XW = Cfg::XW, FPW = Cfg::FPW;
@@ -1344,9 +1383,7 @@ __global__ void __launch_bounds__(256, 2) fused_smallc_kernel(
 #pragma unroll
         for (int f = 0; f < FPW; ++f) {
           if (k0 + f >= kn) break;
-          const int k = k_base + k0 + f;
-          T* dst = y + ((static_cast<size_t>(n) * K + k) * oh + M * ty) * ow + M * t;
-          store_tile<M>(dst, ow, vr, vc, out[f]);
+          emit_tile<M>(y, act, n, K, k_base + k0 + f, oh, ow, ty, t, vr, vc, out[f]);
         }
       }
     }
@@ -1356,7 +1393,7 @@ __global__ void __launch_bounds__(256, 2) fused_smallc_kernel(
 template <int M, typename T, int CE>
 static cudaError_t smallc_one(int prec, const void* d, const void* U, void* y, int N, int C,
                               int H, int W, int K, int pad, int th, int tw, int oh, int ow,
-                              int c_pad, cudaStream_t s) {
+                              int c_pad, cudaStream_t s, int act) {
   using Cfg = SmallCfg<M, T>;
   auto kern = fused_smallc_kernel<M, T, CE>;
   constexpr size_t smem =
@@ -1387,7 +1424,7 @@ static cudaError_t smallc_one(int prec, const void* d, const void* U, void* y, i
     if (per_kc < 1) per_kc = 1;
     const dim3 grid(static_cast<unsigned>(per_kc * nkc));
     launch_k(kern, grid, dim3(256), smem, s, static_cast<const T*>(d), U, static_cast<T*>(y),
-             prec, C, H, W, K, pad, th, tw, oh, ow, c_pad, static_cast<int>(units), nkc);
+             prec, C, H, W, K, pad, th, tw, oh, ow, c_pad, static_cast<int>(units), nkc, act);
     return cudaGetLastError();
   }
 }
@@ -1395,25 +1432,25 @@ static cudaError_t smallc_one(int prec, const void* d, const void* U, void* y, i
 template <int M, typename T>
 static cudaError_t smallc_ce(int prec, const void* d, const void* U, void* y, int N, int C, int H,
                              int W, int K, int pad, int th, int tw, int oh, int ow, int c_pad,
-                             cudaStream_t s) {
+                             cudaStream_t s, int act) {
   switch (C) {
-    case 1: return smallc_one<M, T, 1>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
-    case 2: return smallc_one<M, T, 2>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
-    case 3: return smallc_one<M, T, 3>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
-    case 4: return smallc_one<M, T, 4>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
-    default: return smallc_one<M, T, 8>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
+    case 1: return smallc_one<M, T, 1>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s, act);
+    case 2: return smallc_one<M, T, 2>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s, act);
+    case 3: return smallc_one<M, T, 3>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s, act);
+    case 4: return smallc_one<M, T, 4>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s, act);
+    default: return smallc_one<M, T, 8>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s, act);
   }
 }
 
 cudaError_t launch_fused_smallc(int m, int prec, const void* d, const void* U, void* y, int N,
                                 int C, int H, int W, int K, int pad, int th, int tw, int oh,
-                                int ow, int c_pad, cudaStream_t s) {
+                                int ow, int c_pad, cudaStream_t s, int act) {
   if (C > kSmallC) return cudaErrorInvalidValue;
   if (prec == kFP64)
-    return m == 2 ? smallc_ce<2, double>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s)
-                  : smallc_ce<4, double>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
-  return m == 2 ? smallc_ce<2, float>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s)
-                : smallc_ce<4, float>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s);
+    return m == 2 ? smallc_ce<2, double>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s, act)
+                  : smallc_ce<4, double>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s, act);
+  return m == 2 ? smallc_ce<2, float>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s, act)
+                : smallc_ce<4, float>(prec, d, U, y, N, C, H, W, K, pad, th, tw, oh, ow, c_pad, s, act);
 }
 
 // ====================================================== weight gradient

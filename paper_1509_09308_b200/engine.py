@@ -173,7 +173,7 @@ class WinogradPlan:
         if not x.is_pinned():
             raise ValueError(f"{name} must be in pinned host memory (asynchronous copies)")
 
-    def _operands(self, d, y, U, g, workspace, stream):
+    def _operands(self, d, y, U, g, workspace, stream, out_shape=None):
         """Validate the device operands of one forward; allocate y / workspace when
         absent.  Fresh allocations are made on torch's current stream, so when
         the launch stream differs they are recorded on it (the caching allocator
@@ -192,11 +192,12 @@ class WinogradPlan:
         else:
             self._check_dev(g, (c.K, c.C, c.R, c.S), "g")
         fresh = []
+        out_shape = self.out_shape if out_shape is None else out_shape
         if y is None:
-            y = t.empty(self.out_shape, dtype=self.data_dtype, device=d.device)
+            y = t.empty(out_shape, dtype=self.data_dtype, device=d.device)
             fresh.append(y)
         else:
-            self._check_dev(y, self.out_shape, "y")
+            self._check_dev(y, out_shape, "y")
         if workspace is None:
             workspace = self.alloc_workspace(d.device)
             fresh.append(workspace)
@@ -218,13 +219,27 @@ class WinogradPlan:
     def _ptr(x):
         return x.data_ptr() if x is not None else None
 
-    def forward(self, d, y=None, U=None, g=None, workspace=None, stream=None):
-        """y = conv(d, g) with the precomputed U (FX) or transforming g in place."""
-        y, workspace = self._operands(d, y, U, g, workspace, stream)
-        _lib.check(_lib.lib.wino_forward(
-            self._h, d.data_ptr(), self._ptr(U), g.data_ptr() if U is None else None,
-            y.data_ptr(), workspace.data_ptr(), workspace.numel() * workspace.element_size(),
-            _stream_handle(stream)), "wino_forward")
+    ACTS = {None: 0, "relu": 1, "relu_pool": 2}
+
+    def act_shape(self, act=None):
+        """Output shape of forward(act=...): relu_pool halves out_h and out_w."""
+        N, K, oh, ow = self.out_shape
+        return (N, K, oh // 2, ow // 2) if act == "relu_pool" else (N, K, oh, ow)
+
+    def forward(self, d, y=None, U=None, g=None, workspace=None, stream=None, act=None):
+        """y = conv(d, g) with the precomputed U (FX) or transforming g in place.
+        act="relu" / "relu_pool" fuses max(y, 0) / relu + 2x2 max-pool into the
+        output transform's stores (wino_forward_act)."""
+        if act not in self.ACTS:
+            raise ValueError(f"act must be one of {list(self.ACTS)}, got {act!r}")
+        y, workspace = self._operands(d, y, U, g, workspace, stream, self.act_shape(act))
+        args = (self._h, d.data_ptr(), self._ptr(U), g.data_ptr() if U is None else None,
+                y.data_ptr(), workspace.data_ptr(), workspace.numel() * workspace.element_size())
+        if act is None:
+            _lib.check(_lib.lib.wino_forward(*args, _stream_handle(stream)), "wino_forward")
+        else:
+            _lib.check(_lib.lib.wino_forward_act(*args, self.ACTS[act], _stream_handle(stream)),
+                       "wino_forward_act")
         return y
 
     def forward_timed(self, d, y, timer: "StageTimer", U=None, g=None, workspace=None,

@@ -9,6 +9,11 @@ and a 2x2 / stride-2 max-pool closing each block (224 -> 112 -> 56 -> 28 -> 14
 ``wino_relu_pool``.  Weights are U[-1, 1) scaled by sqrt(3 / (9 C)) (unit
 output variance per layer, so activations stay O(1) through 16 layers).
 Activations are fp32 NCHW, the reference's data type.
+
+The ReLU and the pool are fused into each conv's output transform
+(``wino_forward_act``): the conv writes relu(y), or the pooled relu(y), so no
+separate pass re-reads the activations (``fuse_act=False`` keeps the separate
+``wino_relu_pool`` pass).
 """
 from __future__ import annotations
 
@@ -40,9 +45,10 @@ class VGGEStack:
     """One network-E conv stack at batch N on the current CUDA device."""
 
     def __init__(self, N: int, m: int = 2, prec: str = "fp32", seed: int = 0,
-                 workspace_limit: int = 0) -> None:
+                 workspace_limit: int = 0, fuse_act: bool = True) -> None:
         import torch
         self.N, self.m, self.prec = N, m, prec
+        self.fuse_act = fuse_act
         self.layers = []
         gen = torch.Generator(device="cpu").manual_seed(seed)
         act_max = N * 3 * 224 * 224
@@ -71,7 +77,7 @@ class VGGEStack:
 
     def launches(self) -> int:
         return sum(p.info["launches_per_forward"] + (0 if p.info["combined_transforms"] else 1)
-                   + 1 for (_, _, p, _, _) in self.layers)
+                   + (0 if self.fuse_act else 1) for (_, _, p, _, _) in self.layers)
 
     def forward(self, x, out=None, stream=None):
         """x: (N, 3, 224, 224) fp32 CUDA tensor -> (N, 512, 7, 7)."""
@@ -82,14 +88,19 @@ class VGGEStack:
         cur = x.contiguous()
         bufs = (self._a, self._b)
         for i, (name, cfg, plan, g, pool) in enumerate(self.layers):
-            y = self._c[: cfg.N * cfg.K * cfg.H * cfg.W].view(cfg.N, cfg.K, cfg.H, cfg.W)
-            plan.forward(cur, y=y, g=g, workspace=self._ws, stream=stream)
             oh = cfg.H // 2 if pool else cfg.H
             last = i + 1 == len(self.layers)
             nxt = (out if (last and out is not None) else
                    bufs[(i + 1) % 2][: cfg.N * cfg.K * oh * oh].view(cfg.N, cfg.K, oh, oh))
-            _lib.check(_lib.lib.wino_relu_pool(y.data_ptr(), nxt.data_ptr(), cfg.N, cfg.K, cfg.H,
-                                               cfg.W, 1 if pool else 0, sh), "relu_pool")
+            if self.fuse_act:  # relu (+ pool) in the output transform's stores
+                plan.forward(cur, y=nxt, g=g, workspace=self._ws, stream=stream,
+                             act="relu_pool" if pool else "relu")
+            else:
+                y = self._c[: cfg.N * cfg.K * cfg.H * cfg.W].view(cfg.N, cfg.K, cfg.H, cfg.W)
+                plan.forward(cur, y=y, g=g, workspace=self._ws, stream=stream)
+                _lib.check(_lib.lib.wino_relu_pool(y.data_ptr(), nxt.data_ptr(), cfg.N, cfg.K,
+                                                   cfg.H, cfg.W, 1 if pool else 0, sh),
+                           "relu_pool")
             cur = nxt
         return cur
 
