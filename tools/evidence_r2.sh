@@ -6,6 +6,7 @@ set -u
 OUT=gpurun_out/$1; mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/smi.txt
 T="timeout -s KILL"
+$T 1500 python -m pytest tests/ -m gpu -q > $OUT/gputest.log 2>&1; tail -2 $OUT/gputest.log
 $T 400 python bench.py > $OUT/bench_default.json 2> $OUT/bench_default.err
 for a in "f4x4 fp16 1" "f4x4 fp16 8" "f4x4 fp16 64" "f4x4 bf16 1" "f4x4 bf16 8" "f4x4 bf16 64" "f4x4 tf32 8" "f4x4 tf32 64" "f2x2 fp32 64"; do
   set -- $a
@@ -14,6 +15,9 @@ done
 $T 400 python bench.py --algo f4x4 --prec fp16 --batch 8 --global-batch 64 --no-cpu-baseline --steps 10 > $OUT/bench_f4x4_fp16_global64_1gpu.json 2>> $OUT/bench_other.err
 $T 400 python bench.py --chained --no-cpu-baseline > $OUT/bench_chained_f2_fp32_n1.json 2>> $OUT/bench_other.err
 $T 400 python bench.py --chained --algo f4x4 --prec fp16 --batch 64 --no-cpu-baseline --steps 10 > $OUT/bench_chained_f4_fp16_n64.json 2>> $OUT/bench_other.err
+$T 400 python bench.py --chained --algo f4x4 --prec bf16 --batch 64 --no-cpu-baseline --steps 10 > $OUT/bench_chained_f4_bf16_n64.json 2>> $OUT/bench_other.err
+$T 400 python bench.py --chained --algo f4x4 --prec bf16 --batch 8 --no-cpu-baseline --steps 20 > $OUT/bench_chained_f4_bf16_n8.json 2>> $OUT/bench_other.err
+$T 400 python bench.py --chained --no-fuse-act --no-cpu-baseline > $OUT/bench_chained_f2_fp32_n1_separate_relu.json 2>> $OUT/bench_other.err
 $T 400 python bench.py --workspace 16777216 --no-cpu-baseline > $OUT/bench_default_ws16m.json 2>> $OUT/bench_other.err
 $T 400 python bench.py --algo f4x4 --prec fp16 --batch 64 --workspace 16777216 --no-cpu-baseline --steps 10 > $OUT/bench_f4x4_fp16_n64_ws16m.json 2>> $OUT/bench_other.err
 $T 400 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_reference.json 2> $OUT/bench_reference.err
