@@ -589,7 +589,15 @@ def run_chained(args) -> None:
     prec = args.prec or prec or "fp32"
     if fx:
         raise SystemExit("--chained runs the non-FX forward (filters transformed every step)")
-    B = args.batch
+    strong = args.global_batch > 0  # config 4: a fixed global batch split over the ranks
+    if strong:
+        from paper_1509_09308_b200 import sharding
+        _, B = sharding.shard_bounds(args.global_batch, world, rank)
+        if B <= 0:
+            raise SystemExit(f"--global-batch {args.global_batch} leaves rank {rank} empty")
+    else:
+        B = args.batch
+    images_job = args.global_batch if strong else B * world
     net = VGGEStack(B, m, prec, seed=0, workspace_limit=args.workspace,
                     fuse_act=not args.no_fuse_act)
     gen = torch.Generator(device="cpu").manual_seed(1234 + rank)
@@ -634,7 +642,8 @@ def run_chained(args) -> None:
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_max = float(t.item())
-    value = net.gflop * world * args.steps / t_max / 1e3
+    gf_job = net.gflop / B * images_job  # direct-conv GFLOP of the whole job per step
+    value = gf_job * args.steps / t_max / 1e3
 
     # per-layer stage roofline on the stack's own layer inputs
     entries = []
@@ -660,18 +669,21 @@ def run_chained(args) -> None:
     te = torch.tensor([ea.elapsed_time(eb) / 1e3], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_val = net.gflop * world * e2e_steps / float(te.item()) / 1e3
+    e2e_val = gf_job * e2e_steps / float(te.item()) / 1e3
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOPS",
-            "images_per_s": B * world * args.steps / t_max, "n_gpus": world,
+            "images_per_s": images_job * args.steps / t_max, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": prec, "data": "synthetic",
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": prec,
+            "data": "synthetic",
             "config": {"workload": f"VGG-E conv stack chained as a network (16 conv + ReLU, "
                                    f"2x2 max-pool per block), {args.algo} F({m}x{m},3x3), "
-                                   f"GEMM {prec}, N={B} per GPU",
-                       "algo": args.algo, "global_batch": B * world, "batch_per_gpu": B,
+                                   f"GEMM {prec}, "
+                                   + (f"global N={args.global_batch} split over {world} GPU(s)"
+                                      if strong else f"N={B} per GPU"),
+                       "algo": args.algo, "global_batch": images_job, "batch_per_gpu": B,
                        "parallelism": f"dp{world} batch-shard (no collective)",
                        "l2": f"flushed between timed steps ({args.flush_mb} MB write)",
                        "cuda_graph": True, "chained": True,
