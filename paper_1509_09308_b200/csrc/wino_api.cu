@@ -301,7 +301,18 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
   p->gemm_tr = 0;
   static const long long tr_maxp =
       getenv("WINO_GEMM_TR_MAXP") ? atoll(getenv("WINO_GEMM_TR_MAXP")) : 256;
-  if (prec == kFP32 && gemm_tmem_a_enabled() && !p->smallc && p->P <= tr_maxp &&
+  // The single-pass GEMMs (tf32 / bf16 / fp16) take the same orientation for
+  // K > P <= 64 (their 128-row tile blocks would otherwise carry 16-49 real
+  // tiles: conv4-5 at N = 1): VGG-E F4 N=1 tf32 0.324 -> 0.289 ms, fp16 0.278
+  // -> 0.268, bf16 0.277 -> 0.268; at P = 128 (conv5, N = 8) it measured 1%
+  // slower.  WINO_NO_GEMM_TR16=1 disables, WINO_GEMM_TR16_MAXP moves the bound.
+  const bool tr16 = getenv("WINO_NO_GEMM_TR16") == nullptr;  // (read per plan: tests toggle it)
+  static const long long tr16_maxp =
+      getenv("WINO_GEMM_TR16_MAXP") ? atoll(getenv("WINO_GEMM_TR16_MAXP")) : 64;
+  const bool single_pass = prec == kTF32 || prec == kBF16 || prec == kFP16;
+  const bool tr_prec = (prec == kFP32 && gemm_tmem_a_enabled()) ||
+                       (tr16 && single_pass && p->P <= tr16_maxp);
+  if (tr_prec && !p->smallc && p->P <= tr_maxp &&
       static_cast<long long>(L.K) > p->P && L.K >= 128 && getenv("WINO_NO_GEMM_TR") == nullptr) {
     p->gemm_tr = 1;
     p->bn = p->P <= 32 ? 32 : p->P <= 64 ? 64 : 128;
@@ -366,7 +377,7 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
   }
   // gemm_tr plans take V from the input transform as tf32 hi / lo planes, so
   // the GEMM's B operand needs no on-chip split (WINO_NO_VSPLIT=1 disables)
-  p->v_split2 = (p->gemm_tr && getenv("WINO_NO_VSPLIT") == nullptr) ? 1 : 0;
+  p->v_split2 = (p->gemm_tr && prec == kFP32 && getenv("WINO_NO_VSPLIT") == nullptr) ? 1 : 0;
   p->v_bytes = p->smallc ? 0
                         : align_up(static_cast<size_t>(p->nsplit) * (p->v_split2 ? 2 : 1) *
                                        p->a2 * p->chunk_tiles * p->c_pad * p->esize,
@@ -464,7 +475,8 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
   // (WINO_M16_SMALL=1 stages them in 16 bits too, as a multi-chunk plan would)
   const bool small_f4 = m == 4 && p->num_chunks == 1 && p->chunk_tiles <= output_tma_min_tiles() &&
                         getenv("WINO_M16_SMALL") == nullptr;
-  p->m_bf16 = (p->m_es == 2 && p->splits == 1 && !p->smallc && p->path == kPathStaged && !small_f4)
+  p->m_bf16 = (p->m_es == 2 && p->splits == 1 && !p->smallc && p->path == kPathStaged && !small_f4 &&
+               !p->gemm_tr)  // (the transposed epilogue stores fp32 M)
                   ? (prec == kFP16 ? 2 : 1) : 0;
   if (!p->m_bf16) p->m_es = p->acc_bytes;
   // Non-FX 3xTF32 staged plans: the filter transform writes U as hi / lo planes
@@ -495,7 +507,7 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
     while (p->splits > 1 && p->nbuf * (p->v_bytes + p->m_bytes) + p->ypart_bytes > workspace_limit) {
       const int kbps = (num_kb + p->splits - 2) / (p->splits - 1);
       p->splits = (num_kb + kbps - 1) / kbps;
-      if (p->splits == 1 && m16 && !p->smallc && !small_f4 &&
+      if (p->splits == 1 && m16 && !p->smallc && !small_f4 && !p->gemm_tr &&
           p->path == kPathStaged) {
         p->m_es = 2;
         p->m_bf16 = prec == kFP16 ? 2 : 1;

@@ -871,7 +871,7 @@ template <int PREC, int BN, bool TA, bool MB = false, bool BS = false, bool TRN 
 static cudaError_t launch_tc(const GemmArgs& a, cudaStream_t s) {
   using Tr = GemmTraits<PREC>;
   using Sm = GemmSmem<PREC, BN, TA>;
-  static_assert(!TRN || (TA && !MB), "TRN: 3xTF32 TMEM-A, fp32 M");
+  static_assert(!TRN || !MB, "TRN: fp32 M");
   alignas(64) CUtensorMap tmV, tmU;  // the A (128-row) and B (BN-row) operand maps
   const uint64_t es = Tr::esize;
   const uint64_t planes = static_cast<uint64_t>(op_splits(PREC)) * a.a2;  // planes in HBM
@@ -928,6 +928,16 @@ bool gemm_tmem_a_enabled() { return getenv("WINO_NO_TMEM_A") == nullptr; }
 
 template <int PREC>
 static cudaError_t launch_prec(const GemmArgs& a, cudaStream_t s) {
+  if constexpr (PREC != kFP32) {  // single-pass GEMMs with the filters on the M side
+    if (a.tr) {
+      switch (a.bn) {
+        case 32: return launch_tc<PREC, 32, false, false, false, true>(a, s);
+        case 64: return launch_tc<PREC, 64, false, false, false, true>(a, s);
+        case 128: return launch_tc<PREC, 128, false, false, false, true>(a, s);
+        default: return cudaErrorInvalidValue;
+      }
+    }
+  }
   if constexpr (PREC == kFP32) {  // 3xTF32: A operand through tensor memory (BN <= 128)
     static const bool tmem_a = getenv("WINO_NO_TMEM_A") == nullptr;
     static const bool pair = getenv("WINO_GEMM_2SM") != nullptr;

@@ -528,3 +528,32 @@ def test_grad_inputs_vgg_size(wb, m, C, H, K, pad):
     dd = wb.winograd_grad_inputs(T(dy), T(g), cfg, wb.builtin(m, 3)).data
     assert dd.shape == (1, C, H, H)
     assert O.max_abs_error(dd, _grad_inputs_ref(dy, g, pad)) < (5e-4 if m == 2 else 5e-3)
+
+
+@pytest.mark.parametrize("m", [2, 4])
+@pytest.mark.parametrize("N,C,H,K", [(1, 512, 14, 512), (1, 96, 15, 300), (2, 40, 10, 136)])
+@pytest.mark.parametrize("prec", ["tf32", "bf16", "fp16"])
+def test_single_pass_transposed_gemm(wb, monkeypatch, m, N, C, H, K, prec):
+    """tf32 / bf16 / fp16 plans with K > P <= 64 put the filters on the MMA's
+    128-row side (the 3xTF32 TRN orientation, fp32 M): same gates as the default
+    orientation, which WINO_NO_GEMM_TR16=1 restores."""
+    import torch
+    monkeypatch.setenv("WINO_PATH", "staged")
+    cfg = wb.LayerConfig(N=N, C=C, H=H, W=H, K=K, pad=1)
+    plan = wb.WinogradPlan(cfg, m, prec)
+    P = plan.info["P"]
+    if P > 64:
+        pytest.skip(f"P = {P} > 64: default orientation")
+    assert plan.info["gemm_bn"] in (32, 64) and plan.info["m_bytes_per_elem"] == 4
+    d = O.fill_uniform((N, C, H, H), 71)
+    g = O.fill_uniform((K, C, 3, 3), 72)
+    dd, gg = torch.from_numpy(d).cuda(), torch.from_numpy(g).cuda()
+    y = plan.forward(dd, g=gg).cpu().numpy()
+    ref = O.direct_forward(d, g, 1)
+    scale = np.abs(ref).max()
+    err = O.max_abs_error(y, ref) / scale
+    assert err <= REL_TOL[(prec, m)], err
+    monkeypatch.setenv("WINO_NO_GEMM_TR16", "1")
+    y0 = wb.WinogradPlan(cfg, m, prec).forward(dd, g=gg).cpu().numpy()
+    err0 = O.max_abs_error(y0, ref) / scale
+    assert err <= 1.5 * err0 + 1e-6, (err, err0)

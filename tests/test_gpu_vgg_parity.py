@@ -224,9 +224,12 @@ def test_batched_plans_image0_and_slices(wb, fx, monkeypatch, i, N, prec, m):
     lbl, C, H, K = LAYERS[i]
     if N * C * H * H > 64 * 512 * 112 * 112:
         pytest.skip("input > 1.6 GB")
-    # a single small F(4x4) chunk keeps fp32 M by default; stage M in 16 bits in
-    # both plans so that only chunking and ordering differ between them
+    # a single small F(4x4) chunk keeps fp32 M by default, and a 16-bit plan of
+    # <= 64 tiles with K > P puts the filters on the MMA side (fp32 M); stage M
+    # in 16 bits in both plans, in the same GEMM orientation, so that only
+    # chunking and ordering differ between them
     monkeypatch.setenv("WINO_M16_SMALL", "1")
+    monkeypatch.setenv("WINO_NO_GEMM_TR16", "1")
     d, g, y64 = _batch(i, N)
     cfg = wb.LayerConfig(N=N, C=C, H=H, W=H, K=K, pad=1)
     plan, y = _run(wb, cfg, m, prec, d, g)
