@@ -90,11 +90,10 @@ __device__ __forceinline__ void emit_tile(TA* __restrict__ y, int act, int n, in
     for (int i = 0; i < P; ++i)
 #pragma unroll
       for (int j = 0; j < P; ++j) {
-        const TA a = out[2 * i][2 * j] > out[2 * i][2 * j + 1] ? out[2 * i][2 * j] : out[2 * i][2 * j + 1];
-        const TA b = out[2 * i + 1][2 * j] > out[2 * i + 1][2 * j + 1] ? out[2 * i + 1][2 * j]
-                                                                         : out[2 * i + 1][2 * j + 1];
-        const TA v = a > b ? a : b;
-        pooled[i][j] = v < TA(0) ? TA(0) : v;
+        // fmax semantics, as the separate wino_relu_pool pass (wino_net.cu)
+        const TA a = fmax(out[2 * i][2 * j], out[2 * i][2 * j + 1]);
+        const TA b = fmax(out[2 * i + 1][2 * j], out[2 * i + 1][2 * j + 1]);
+        pooled[i][j] = fmax(fmax(a, b), TA(0));
       }
     const int ph = oh >> 1, pw = ow >> 1;
     TA* dst = y + ((static_cast<size_t>(n) * K + k) * ph + P * ty) * pw + P * tx;
@@ -105,7 +104,7 @@ __device__ __forceinline__ void emit_tile(TA* __restrict__ y, int act, int n, in
 #pragma unroll
     for (int i = 0; i < M; ++i)
 #pragma unroll
-      for (int j = 0; j < M; ++j) out[i][j] = out[i][j] < TA(0) ? TA(0) : out[i][j];
+      for (int j = 0; j < M; ++j) out[i][j] = fmax(out[i][j], TA(0));
   }
   TA* dst = y + ((static_cast<size_t>(n) * K + k) * oh + M * ty) * ow + M * tx;
   store_tile<M>(dst, ow, vr, vc, out);
