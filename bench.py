@@ -587,8 +587,6 @@ def run_chained(args) -> None:
         dist.init_process_group("nccl", device_id=dev)
     m, fx, prec = wb.parse_algo(args.algo)
     prec = args.prec or prec or "fp32"
-    if fx:
-        raise SystemExit("--chained runs the non-FX forward (filters transformed every step)")
     strong = args.global_batch > 0  # config 4: a fixed global batch split over the ranks
     if strong:
         from paper_1509_09308_b200 import sharding
@@ -599,7 +597,7 @@ def run_chained(args) -> None:
         B = args.batch
     images_job = args.global_batch if strong else B * world
     net = VGGEStack(B, m, prec, seed=0, workspace_limit=args.workspace,
-                    fuse_act=not args.no_fuse_act)
+                    fuse_act=not args.no_fuse_act, fx=fx)
     gen = torch.Generator(device="cpu").manual_seed(1234 + rank)
     x_host = (torch.rand(net.in_shape, generator=gen) * 2 - 1).pin_memory()
     x = x_host.to(dev)
@@ -647,11 +645,11 @@ def run_chained(args) -> None:
 
     # per-layer stage roofline on the stack's own layer inputs
     entries = []
-    for (name, cfg, plan, g, pool) in net.layers:
+    for i, (name, cfg, plan, g, pool) in enumerate(net.layers):
         d = torch.rand((cfg.N, cfg.C, cfg.H, cfg.W), device=dev)
         y = torch.empty(plan.out_shape, device=dev)
-        entries.append((cfg, plan, d, y, net._ws, None, g, 1))
-    roof = stage_roofline(entries, prec, False, stream, flush, args.algo, B)
+        entries.append((cfg, plan, d, y, net._ws, net._U[i] if fx else None, g, 1))
+    roof = stage_roofline(entries, prec, fx, stream, flush, args.algo, B)
 
     # e2e: pinned input -> device, the stack, output -> pinned host, every step
     e2e_steps = max(1, min(args.steps, 10))
@@ -688,7 +686,9 @@ def run_chained(args) -> None:
                        "l2": f"flushed between timed steps ({args.flush_mb} MB write)",
                        "cuda_graph": True, "chained": True,
                        "relu_pool": "separate pass" if args.no_fuse_act else
-                       "fused into the output transform (wino_forward_act)"},
+                       "fused into the output transform (wino_forward_act)",
+                       "filters": "transformed once (FX, FilterCache semantics)" if fx else
+                       "transformed every step (non-FX)"},
             "roofline": roof,
             "cpu_baseline": None,
             "e2e": {"value": e2e_val, "unit": "TFLOPS",

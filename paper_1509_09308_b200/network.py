@@ -45,10 +45,11 @@ class VGGEStack:
     """One network-E conv stack at batch N on the current CUDA device."""
 
     def __init__(self, N: int, m: int = 2, prec: str = "fp32", seed: int = 0,
-                 workspace_limit: int = 0, fuse_act: bool = True) -> None:
+                 workspace_limit: int = 0, fuse_act: bool = True, fx: bool = False) -> None:
         import torch
         self.N, self.m, self.prec = N, m, prec
         self.fuse_act = fuse_act
+        self.fx = fx  # FX: filters transformed once here, like the reference's FilterCache
         self.layers = []
         gen = torch.Generator(device="cpu").manual_seed(seed)
         act_max = N * 3 * 224 * 224
@@ -68,6 +69,7 @@ class VGGEStack:
         self._b = torch.empty(act_max, dtype=torch.float32, device="cuda")
         self._c = torch.empty(act_max, dtype=torch.float32, device="cuda")
         self._ws = torch.empty(ws_max, dtype=torch.uint8, device="cuda")
+        self._U = [plan.filter_transform(g) if fx else None for (_, _, plan, g, _) in self.layers]
         last = self.layers[-1][1]
         self.out_shape = (N, last.K, last.H // 2, last.W // 2)
 
@@ -76,7 +78,8 @@ class VGGEStack:
         return (self.N, 3, 224, 224)
 
     def launches(self) -> int:
-        return sum(p.info["launches_per_forward"] + (0 if p.info["combined_transforms"] else 1)
+        return sum(p.info["launches_per_forward"]
+                   + (0 if (self.fx or p.info["combined_transforms"]) else 1)
                    + (0 if self.fuse_act else 1) for (_, _, p, _, _) in self.layers)
 
     def forward(self, x, out=None, stream=None):
@@ -92,12 +95,13 @@ class VGGEStack:
             last = i + 1 == len(self.layers)
             nxt = (out if (last and out is not None) else
                    bufs[(i + 1) % 2][: cfg.N * cfg.K * oh * oh].view(cfg.N, cfg.K, oh, oh))
+            wg = dict(U=self._U[i]) if self.fx else dict(g=g)
             if self.fuse_act:  # relu (+ pool) in the output transform's stores
-                plan.forward(cur, y=nxt, g=g, workspace=self._ws, stream=stream,
-                             act="relu_pool" if pool else "relu")
+                plan.forward(cur, y=nxt, workspace=self._ws, stream=stream,
+                             act="relu_pool" if pool else "relu", **wg)
             else:
                 y = self._c[: cfg.N * cfg.K * cfg.H * cfg.W].view(cfg.N, cfg.K, cfg.H, cfg.W)
-                plan.forward(cur, y=y, g=g, workspace=self._ws, stream=stream)
+                plan.forward(cur, y=y, workspace=self._ws, stream=stream, **wg)
                 _lib.check(_lib.lib.wino_relu_pool(y.data_ptr(), nxt.data_ptr(), cfg.N, cfg.K,
                                                    cfg.H, cfg.W, 1 if pool else 0, sh),
                            "relu_pool")

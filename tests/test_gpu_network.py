@@ -93,3 +93,16 @@ def test_forward_act_errors(monkeypatch):
     fused = wb.WinogradPlan(wb.LayerConfig(N=1, C=16, H=10, W=10, K=8, pad=1), 2, "fp32")
     with pytest.raises(ValueError):  # the epilogue runs on the staged path only
         fused.forward(torch.rand((1, 16, 10, 10), device="cuda"), g=g, act="relu")
+
+
+def test_fx_stack_equals_non_fx():
+    """fx=True transforms the filters once (FilterCache semantics); the forward
+    with the cached U is bitwise the non-FX forward."""
+    import torch
+    from paper_1509_09308_b200.network import VGGEStack
+    a = VGGEStack(1, 4, "bf16", seed=6, fx=True)
+    b = VGGEStack(1, 4, "bf16", seed=6, fx=False)
+    x = torch.rand(a.in_shape, device="cuda") * 2 - 1
+    ya, yb = a.forward(x), b.forward(x)
+    torch.cuda.synchronize()
+    assert torch.equal(ya, yb)
