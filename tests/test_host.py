@@ -255,3 +255,31 @@ def test_cli_accuracy_usage_errors():
     from paper_1509_09308_b200.__main__ import main
     assert main(["accuracy", "--algos", "fft8"]) == 1
     assert main(["accuracy", "--algos", "f2x2", "--suite", "no-such-suite"]) == 1
+
+
+def test_vgg_e_network_layers():
+    """network E's 16 conv layers in order, with a pool closing each block
+    (PAPER.md:549-563): 224 -> 112 -> 56 -> 28 -> 14 -> 7."""
+    from paper_1509_09308_b200.network import vgg_e_layers
+    layers = vgg_e_layers()
+    assert len(layers) == 16
+    assert [l[0] for l in layers][:3] == ["conv1.1", "conv1.2", "conv2.1"]
+    chans = [(C, K) for (_, C, _, K, _) in layers]
+    assert all(chans[i][1] == chans[i + 1][0] for i in range(15))  # K_i == C_{i+1}
+    pools = [i for i, l in enumerate(layers) if l[4]]
+    assert pools == [1, 3, 7, 11, 15]
+    sizes = [H for (_, _, H, _, _) in layers]
+    for i in pools[:-1]:
+        assert sizes[i + 1] == sizes[i] // 2
+
+
+def test_forward_act_shapes_and_validation():
+    """act="relu_pool" halves the output plane; unknown activations are rejected
+    before any launch (plan creation needs no GPU)."""
+    import paper_1509_09308_b200 as wb
+    plan = wb.WinogradPlan(wb.LayerConfig(N=2, C=16, H=28, W=28, K=8, pad=1), 4, "fp32")
+    assert plan.act_shape(None) == plan.out_shape == (2, 8, 28, 28)
+    assert plan.act_shape("relu") == (2, 8, 28, 28)
+    assert plan.act_shape("relu_pool") == (2, 8, 14, 14)
+    with pytest.raises(ValueError):
+        plan.forward(None, act="gelu")
