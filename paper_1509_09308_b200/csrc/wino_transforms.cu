@@ -1192,22 +1192,30 @@ __device__ __forceinline__ float load_op_any(int prec, const void* U, size_t idx
 }
 
 // FPW filters per warp for vector weight loads (F(2x2)'s 2x2 outputs leave
-// registers for 8, F(4x4)'s 4x4 for 4).
+// registers for 8; F(4x4)'s 4x4 outputs fit 2 without spilling at two CTAs
+// per SM -- four spilled 24 B per thread: conv1.1 F4 N=64 303 -> 288 us).
 template <int M, typename T>
 struct SmallCfg {
   static constexpr int AL = M + 2, A2 = AL * AL, XW = kSmallTiles * M + 2;
-  static constexpr int FPW = (M == 2 && sizeof(T) == 4) ? 8 : 4;
+  static constexpr int FPW = (M == 2 && sizeof(T) == 4) ? 8 : 2;
   static constexpr int passes = kSmallKC / (8 * FPW);
 };
 
 // FPW consecutive fp32 / fp64 values (16-byte aligned), broadcast loads
 template <typename T, int FPW>
 __device__ __forceinline__ void load_u(const T* p, T (&u)[FPW]) {
-  if constexpr (sizeof(T) == 4) {
+  if constexpr (sizeof(T) == 4 && FPW % 4 == 0) {
 #pragma unroll
     for (int q = 0; q < FPW / 4; ++q) {
       const float4 x = reinterpret_cast<const float4*>(p)[q];
       u[4 * q] = x.x; u[4 * q + 1] = x.y; u[4 * q + 2] = x.z; u[4 * q + 3] = x.w;
+    }
+  } else if constexpr (sizeof(T) == 4) {
+    static_assert(FPW % 2 == 0, "FPW");
+#pragma unroll
+    for (int q = 0; q < FPW / 2; ++q) {
+      const float2 x = reinterpret_cast<const float2*>(p)[q];
+      u[2 * q] = x.x; u[2 * q + 1] = x.y;
     }
   } else {
 #pragma unroll
