@@ -181,6 +181,30 @@ int wino_forward_act(wino_plan_t plan, const void* d, const void* U, const void*
  * y is (N,C,H/2,W/2)).  fp32 device pointers, enqueued on `stream`. */
 int wino_relu_pool(const float* x, float* y, int N, int C, int H, int W, int pool, void* stream);
 
+/* Batch shards over several GPUs from one host thread (SURVEY.md §8(b)
+ * `wino_forward_sharded`, §8(e); the one-process-per-GPU torch.distributed
+ * driver is sharding.py).  Images are independent: shard s of n_shards holds
+ * the contiguous images [start, start + count) of the plan's N -- the first
+ * N % n_shards shards take one extra, as sharding.shard_bounds -- and runs on
+ * devices[s].  No data crosses devices (outputs stay sharded, no collective). */
+int wino_shard_bounds(int N, int n_shards, int shard, int* start, int* count);
+/* Bytes shard s's workspace needs: with_filters != 0 for a forward that
+ * transforms g itself, 0 when U is passed.  0 for a shard without images. */
+int wino_shard_workspace(wino_plan_t plan, int n_shards, int shard, int with_filters,
+                         size_t* bytes);
+/* Enqueue every shard's forward of `plan` (the full layer).  Per shard s, on
+ * devices[s] (several shards may share a device): d[s] (count, C, H, W),
+ * y[s] (count, K, out_h, out_w), U[s] = wino_filter_transform(plan, ...) on that
+ * device, or U == NULL and g[s] (K, C, 3, 3); workspace[s] of
+ * workspace_bytes[s] >= wino_shard_workspace; streams[s] (streams == NULL:
+ * each device's legacy stream).  Shards without images are skipped (their
+ * pointers may be NULL).  The calling thread's current device is restored.
+ * Returns after enqueueing; on error the message names the shard. */
+int wino_forward_sharded(wino_plan_t plan, int n_shards, const int* devices,
+                         const void* const* d, const void* const* U, const void* const* g,
+                         void* const* y, void* const* workspace, const size_t* workspace_bytes,
+                         void* const* streams);
+
 const char* wino_last_error(void);
 /* Library version string. */
 const char* wino_version(void);

@@ -26,6 +26,7 @@ EXPORTED = ("wino_plan_create", "wino_plan_destroy", "wino_plan_get_info",
             "wino_timer_create", "wino_timer_destroy", "wino_timer_break", "wino_timer_read",
             "wino_wgrad_workspace", "wino_grad_weights", "wino_direct_forward", "wino_relu_pool",
             "wino_fft_workspace", "wino_fft_forward", "wino_forward_act",
+            "wino_shard_bounds", "wino_shard_workspace", "wino_forward_sharded",
             "wino_last_error", "wino_version")
 
 
@@ -88,6 +89,11 @@ def _load() -> ctypes.CDLL:
                                      vp]
     lib.wino_relu_pool.argtypes = [vp, vp, c_int, c_int, c_int, c_int, c_int, vp]
     lib.wino_forward_act.argtypes = [vp, vp, vp, vp, vp, vp, sz, c_int, vp]
+    pint = ctypes.POINTER(c_int)
+    lib.wino_shard_bounds.argtypes = [c_int, c_int, c_int, pint, pint]
+    lib.wino_shard_workspace.argtypes = [vp, c_int, c_int, c_int, ctypes.POINTER(sz)]
+    lib.wino_forward_sharded.argtypes = [vp, c_int, pint] + [ctypes.POINTER(vp)] * 5 + [
+        ctypes.POINTER(sz), ctypes.POINTER(vp)]
     lib.wino_last_error.restype = ctypes.c_char_p
     lib.wino_version.restype = ctypes.c_char_p
     for name in EXPORTED:

@@ -39,6 +39,7 @@ struct wino_plan_s {
   int v_split2;                      // with gemm_tr: V written as tf32 hi / lo planes
   size_t u_ws;                       // workspace bytes of a forward-computed U
   size_t staging_bytes;              // V + M of the chunks in flight (+ fused partials)
+  size_t ws_limit;                   // workspace_limit passed at creation (shard sub-plans)
 };
 
 namespace wino {
@@ -256,6 +257,7 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
     return WINO_ENOMEM;
   }
   p->L = L;
+  p->ws_limit = workspace_limit;
   p->m = m;
   p->r = 3;
   p->alpha = m + 2;
@@ -956,6 +958,98 @@ int wino_forward_host(wino_plan_t p, const void* d_host, const void* U, const vo
   e = cudaMemcpyAsync(y_host, y_dev, yb, cudaMemcpyDeviceToHost, s);
   if (e != cudaSuccess) return cuda_fail(e, "D2H copy");
   return WINO_OK;
+}
+
+// ---------------------------------------------------------------- batch shards
+// Multi-GPU from one host thread (SURVEY.md §8(b) wino_forward_sharded, §8(e)):
+// images are independent, so shard s runs the layer on its contiguous images
+// with a sub-plan of batch `count` on devices[s]; no data crosses devices.  The
+// U layout depends only on (m, prec, K, C), so the full plan's filter
+// transform serves every sub-plan.  Sub-plans are built per call (host-only
+// planning) and freed before returning; kernels already enqueued keep running.
+int wino_shard_bounds(int N, int n_shards, int shard, int* start, int* count) {
+  g_err.clear();
+  if (!start || !count) {
+    set_error("null argument");
+    return WINO_EINVAL;
+  }
+  if (n_shards < 1 || shard < 0 || shard >= n_shards) {
+    set_error("bad shard %d of %d", shard, n_shards);
+    return WINO_EINVAL;
+  }
+  if (N < 0) {
+    set_error("N must be >= 0");
+    return WINO_EINVAL;
+  }
+  const int base = N / n_shards, extra = N % n_shards;  // sharding.shard_bounds
+  *start = shard * base + (shard < extra ? shard : extra);
+  *count = base + (shard < extra ? 1 : 0);
+  return WINO_OK;
+}
+
+static int shard_plan(wino_plan_t p, int n_shards, int shard, wino_plan_t* sub) {
+  *sub = nullptr;
+  int start = 0, count = 0;
+  int rc = wino_shard_bounds(p->L.N, n_shards, shard, &start, &count);
+  if (rc != WINO_OK || count == 0) return rc;
+  wino_layer_t L = p->L;
+  L.N = count;
+  return wino_plan_create(&L, p->m, p->prec, p->ws_limit, sub);
+}
+
+int wino_shard_workspace(wino_plan_t p, int n_shards, int shard, int with_filters,
+                         size_t* bytes) {
+  g_err.clear();
+  if (!p || !bytes) {
+    set_error("null argument");
+    return WINO_EINVAL;
+  }
+  wino_plan_t sub = nullptr;
+  const int rc = shard_plan(p, n_shards, shard, &sub);
+  if (rc != WINO_OK) return rc;
+  *bytes = 0;
+  if (sub) {
+    *bytes = with_filters ? sub->u_ws + sub->nbuf * (sub->v_bytes + sub->m_bytes) + sub->ypart_bytes
+                          : sub->staging_bytes;
+    wino_plan_destroy(sub);
+  }
+  return WINO_OK;
+}
+
+int wino_forward_sharded(wino_plan_t p, int n_shards, const int* devices,
+                         const void* const* d, const void* const* U, const void* const* g,
+                         void* const* y, void* const* workspace, const size_t* workspace_bytes,
+                         void* const* streams) {
+  g_err.clear();
+  if (!p || n_shards < 1 || !devices || !d || !y || !workspace || !workspace_bytes ||
+      (!U && !g)) {
+    set_error("null argument or n_shards < 1");
+    return WINO_EINVAL;
+  }
+  int dev0 = 0;
+  cudaError_t e = cudaGetDevice(&dev0);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  int rc = WINO_OK;
+  for (int s = 0; s < n_shards && rc == WINO_OK; ++s) {
+    e = cudaSetDevice(devices[s]);
+    if (e != cudaSuccess) {
+      rc = cuda_fail(e, "cudaSetDevice");
+      break;
+    }
+    wino_plan_t sub = nullptr;
+    rc = shard_plan(p, n_shards, s, &sub);
+    if (rc != WINO_OK || !sub) continue;  // error, or a shard without images
+    rc = forward_impl(sub, d[s], U ? U[s] : nullptr, g ? g[s] : nullptr, y[s], workspace[s],
+                      workspace_bytes[s], streams ? streams[s] : nullptr, nullptr);
+    wino_plan_destroy(sub);
+    if (rc != WINO_OK) {
+      const std::string msg = g_err;
+      set_error("shard %d (device %d): %s", s, devices[s], msg.c_str());
+    }
+  }
+  e = cudaSetDevice(dev0);
+  if (rc == WINO_OK && e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  return rc;
 }
 
 // ---------------------------------------------------------------- weight gradient

@@ -195,6 +195,29 @@ def test_shard_bounds_partition(N, world):
         pos += c
     assert max(c for _, c in spans) - min(c for _, c in spans) <= 1
 
+    # the C ABI's wino_shard_bounds is the same split (host-only call)
+    assert [sharding.shard_bounds_native(N, world, r) for r in range(world)] == spans
+
+
+def test_shard_abi_errors_and_workspace():
+    import ctypes
+    from paper_1509_09308_b200 import _lib
+    with pytest.raises(ValueError):
+        sharding.shard_bounds_native(8, 0, 0)
+    with pytest.raises(ValueError):
+        sharding.shard_bounds_native(8, 2, 2)
+    cfg = wb.LayerConfig(N=5, C=64, H=28, W=28, K=64, pad=1)
+    plan = engine.WinogradPlan(cfg, 4, "bf16")
+    b = ctypes.c_size_t()
+    for s, cnt in enumerate((2, 2, 1)):
+        sub = engine.WinogradPlan(cfg.with_batch(cnt), 4, "bf16")
+        for with_g, key in ((1, "workspace_bytes"), (0, "staging_bytes")):
+            assert _lib.lib.wino_shard_workspace(plan._h, 3, s, with_g, ctypes.byref(b)) == 0
+            assert b.value == sub.info[key]
+    # a shard without images needs nothing
+    assert _lib.lib.wino_shard_workspace(plan._h, 8, 7, 1, ctypes.byref(b)) == 0 and b.value == 0
+    assert _lib.lib.wino_forward_sharded(plan._h, 0, None, None, None, None, None, None, None,
+                                         None) == _lib.WINO_EINVAL
 
 def test_filter_cache_key_semantics():
     g = rand((2, 3, 3, 3), 1)
