@@ -105,12 +105,15 @@ class DeviceShardedForward:
                                         device=f"cuda:{dev}"))
 
     def set_filters(self, g) -> None:
-        """Replicated filters: U transformed on every shard's device."""
+        """Replicated filters: U transformed on every shard's device, on that
+        device's current stream (the stream forward() enqueues on)."""
         import torch
         self.U = []
         for dev in self.devices:
             with torch.cuda.device(dev):
-                self.U.append(self.plan.filter_transform(g.to(f"cuda:{dev}").contiguous()))
+                self.U.append(self.plan.filter_transform(
+                    g.to(device=f"cuda:{dev}", dtype=self.plan.data_dtype).contiguous(),
+                    stream=torch.cuda.current_stream(dev)))
 
     def forward(self, d_shards, y_shards=None, g=None):
         """d_shards[s]: (count_s, C, H, W) on devices[s] -> list of y shards.
