@@ -288,6 +288,7 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
   if (const char* e = getenv("WINO_GEMM_BN")) {  // tuning override (32/64/128/256)
     const int v = atoi(e);
     if (v == 32 || v == 64 || v == 128 || v == 256) bn = v;
+    if (prec == kFP32 && bn > 128) bn = 128;  // the 3xTF32 kernels stop at 128
   }
   p->bn = bn;
 
