@@ -25,12 +25,15 @@ def _inputs(cfg, seed):
     (4, "fp16", 3, 256, 14, 512, 2),   # K > P on every shard
     (2, "fp32", 2, 3, 32, 64, 4),      # small-C kernel; two shards without images
     (4, "tf32", 64, 512, 14, 512, 8),  # config 4's conv5 split, 8 images per shard
+    (4, "fp64", 3, 16, 12, 8, 2),      # fp64 data on the CUDA-core GEMM
 ])
 def test_sharded_equals_per_shard_plans(m, prec, N, C, H, K, shards):
     """Each shard is bitwise the forward of a plan built for its own batch, FX
     and non-FX, and the gathered output matches the direct convolution."""
     cfg = LayerConfig(N=N, C=C, H=H, W=H, K=K, pad=1)
     d, g = _inputs(cfg, 7)
+    if prec == "fp64":
+        d, g = d.double(), g.double()
     sf = DeviceShardedForward(cfg, m, prec, devices=[0] * shards)
     parts = [d[s:s + c].contiguous() for s, c in sf.bounds]
     sf.set_filters(g)
@@ -48,7 +51,8 @@ def test_sharded_equals_per_shard_plans(m, prec, N, C, H, K, shards):
     y = torch.cat(ys)
     exact = torch.nn.functional.conv2d(d.double(), g.double(), padding=1)
     rel = ((y.double() - exact).abs().max() / exact.abs().max()).item()
-    tol = {("fp32", 2): 5e-5, ("tf32", 4): 4e-2, ("bf16", 4): 1.5e-1, ("fp16", 4): 2.5e-2}
+    tol = {("fp32", 2): 5e-5, ("tf32", 4): 4e-2, ("bf16", 4): 1.5e-1, ("fp16", 4): 2.5e-2,
+           ("fp64", 4): 1e-12}
     assert rel <= tol[(prec, m)], rel  # test_gpu_parity.REL_TOL; fp32 within the 5e-4 gate
 
 
