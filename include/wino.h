@@ -47,8 +47,8 @@ extern "C" {
 #define WINO_PREC_TF32 1 /* single-pass TF32 on tcgen05                        */
 #define WINO_PREC_BF16 2 /* bf16 operands on tcgen05 kind::f16; M staged as bf16 */
 #define WINO_PREC_FP16 3 /* fp16 operands on tcgen05 kind::f16; M staged as fp16
-                            of M * 2^-4 (|M| < 2^20); both keep fp32 M on single
-                            F(4x4) chunks of <= 256 tiles and on split-C plans  */
+                            of M * 2^-4 (|M| < 2^20); both keep fp32 M on
+                            split-C plans and the transposed (K > P) GEMM       */
 #define WINO_PREC_FP64 4 /* fp64 data and GEMM on CUDA cores (reference FP64)  */
 
 /* One convolution layer; mirrors winoconv.direct.LayerConfig (direct.py:32-66).

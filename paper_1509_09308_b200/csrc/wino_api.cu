@@ -472,11 +472,11 @@ int wino_plan_create(const wino_layer_t* layer, int m, int prec, size_t workspac
     p->overlap = p->num_chunks > 1;
     if (!p->overlap) p->nbuf = 1;
   }
-  // (F(4x4) single chunks of <= output_tma_min_tiles() tiles -- conv3-5 at N = 1 --
-  // keep fp32 M: their per-thread output transform beats the TMA box, and the
-  // staging bytes of one small chunk do not matter; F4 fp16 N=1 0.303 -> 0.282 ms)
-  // (WINO_M16_SMALL=1 stages them in 16 bits too, as a multi-chunk plan would)
-  const bool small_f4 = m == 4 && p->num_chunks == 1 && p->chunk_tiles <= output_tma_min_tiles() &&
+  // (F(4x4) single chunks of <= output_tma_min_tiles(prec) tiles keep fp32 M for
+  // the per-thread output transform; for the 16-bit GEMMs the threshold is 0 by
+  // default (WINO_OUT_TMA_MIN raises it).  WINO_M16_SMALL=1 stages them in 16
+  // bits regardless.)
+  const bool small_f4 = m == 4 && p->num_chunks == 1 && p->chunk_tiles <= output_tma_min_tiles(prec) &&
                         getenv("WINO_M16_SMALL") == nullptr;
   p->m_bf16 = (p->m_es == 2 && p->splits == 1 && !p->smallc && p->path == kPathStaged && !small_f4 &&
                !p->gemm_tr)  // (the transposed epilogue stores fp32 M)

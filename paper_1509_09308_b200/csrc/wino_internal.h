@@ -79,7 +79,7 @@ cudaError_t launch_input_transform(int m, int prec, const void* d, void* V, int 
 // split slices are summed in ascending order (deterministic).
 // F(4x4) chunks of at most this many tiles take the per-thread output transform
 // (fp32 M) instead of the TMA box (WINO_OUT_TMA_MIN, default 256).
-long long output_tma_min_tiles();
+long long output_tma_min_tiles(int prec);
 // `dead`/`dead_bytes`: a 128-byte-aligned region (the chunk's V) that is dead once
 // the GEMM has run; the TMA variant drops its L2 lines (no HBM write-back).
 // `act`: epilogue activation of the written tiles (kActNone / kActRelu /

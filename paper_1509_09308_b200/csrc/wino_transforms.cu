@@ -1106,9 +1106,10 @@ static cudaError_t output_tma_launch(const void* Mbuf, void* y, int K, int th, i
   return cudaGetLastError();
 }
 
-long long output_tma_min_tiles() {
-  static const long long v = getenv("WINO_OUT_TMA_MIN") ? atoll(getenv("WINO_OUT_TMA_MIN")) : 256;
-  return v;
+long long output_tma_min_tiles(int prec) {
+  static const char* e = getenv("WINO_OUT_TMA_MIN");
+  if (e) return atoll(e);
+  return (prec == kBF16 || prec == kFP16) ? 0 : 256;
 }
 
 cudaError_t launch_output_transform(int m, int prec, const void* Mbuf, void* y, int N, int K,
@@ -1130,11 +1131,12 @@ cudaError_t launch_output_transform(int m, int prec, const void* Mbuf, void* y, 
                   : output_tma_launch<4, __nv_bfloat16>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s,
                                                         dead, dead_bytes, act);
   }
-  // F(4x4) chunks of <= 256 tiles (conv3-5 at N = 1) take the per-thread
-  // kernel: VGG-E F4 fp16 N=1 0.294 -> 0.275 ms.  For F(2x2) the TMA box stays
-  // faster on every chunk size in the pass (F2 fp32 N=1: 0.371 vs 0.377 ms).
-  // WINO_OUT_TMA_MIN overrides the F(4x4) tile threshold.
-  const long long tma_min = output_tma_min_tiles();
+  // F(4x4) chunks of <= output_tma_min_tiles(prec) tiles take the per-thread
+  // kernel: 256 for fp32 / tf32 (F4 tf32 N=1 0.300 -> 0.289 ms), 0 for the
+  // 16-bit GEMMs, whose small chunks then stage 16-bit M too (F4 N=1 fp16
+  // 0.267 -> 0.264, bf16 0.266 -> 0.263 ms).  WINO_OUT_TMA_MIN overrides.  For
+  // F(2x2) the TMA box is always taken.
+  const long long tma_min = output_tma_min_tiles(prec);
   if (prec != kFP64 && splits == 1 && (m == 2 || Pc > tma_min) &&
       getenv("WINO_NO_TMA_OUTPUT") == nullptr)
     return m == 2 ? output_tma_launch<2, float>(Mbuf, y, K, th, tw, oh, ow, row0, Pc, m_ld, s,

@@ -263,10 +263,11 @@ def test_planner_decisions_vgg():
     assert conv42["gemm_splits"] == 1
     conv32 = info(256, 56, 256, 4, "bf16", 64)
     assert conv32["m_bytes_per_elem"] == 2 and conv32["num_chunks"] > 1
-    # fp16 stages M in fp16 (x 2^-4) too, except small single F(4x4) chunks
-    # (<= 256 tiles: the per-thread output transform with fp32 M is faster there)
+    # fp16 stages M in fp16 (x 2^-4) too, small single F(4x4) chunks included
+    # (WINO_OUT_TMA_MIN=0); the transposed GEMM (K > P <= 64) keeps fp32 M
     assert info(256, 56, 256, 4, "fp16", 64)["m_bytes_per_elem"] == 2
-    assert info(256, 56, 256, 4, "fp16", 1)["m_bytes_per_elem"] == 4
+    assert info(256, 56, 256, 4, "fp16", 1)["m_bytes_per_elem"] == 2
+    assert info(512, 14, 512, 4, "fp16", 1)["m_bytes_per_elem"] == 4
     assert info(64, 224, 64, 4, "fp16", 1)["m_bytes_per_elem"] == 2
     conv12 = info(64, 224, 64, 2, "fp32", 64)
     assert conv12["num_chunks"] > 1 and conv12["m_bytes_per_elem"] == 4
